@@ -1,0 +1,399 @@
+#!/usr/bin/env python3
+"""Benchmark: fused gossip + DAdam step, param-updates/s (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (config.workload): BASELINE.json configs[1]/[4] -- one-peer exponential
+gossip, 8 simulated nodes per B200 (8*N nodes total; N=1 is configs[1] with 8
+nodes on one device, N=8 is configs[4]), 125M-parameter flat fp32 bucket per
+node, DAdam (alpha 2e-3, betas 0.974/0.999).  A "step" is one
+dg_engine_step(t) over every resident node's full bucket: mixing with the
+round-t peers (NCCL send/recv over NVLink for remote peers), Adam moments and
+the model update, in one fused sm_100a kernel per chunk.  Weak scaling: per-GPU
+work is fixed as N grows.
+
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 2410
+METRIC = "gossip+DAdam param-updates/sec"
+UNIT = "param-updates/s"
+HBM_PER_UPDATE = 28.0          # B per DAdam param-update
+HBM_PER_REMOTE = 12.0          # B of HBM per received remote bucket param (send read + slot write + read)
+NVL_MEASURED = 770e9           # B/s per direction, measured peer copy (B200_PROFILING.md)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--nodes-per-gpu", type=int, default=8)
+    p.add_argument("--d", type=int, default=125_000_000)
+    p.add_argument("--topology", default="one_peer_exponential",
+                   choices=["one_peer_exponential", "one_peer_ring", "static_exponential", "aer"])
+    p.add_argument("--algo", choices=["dadam", "accum"], default="dadam")
+    p.add_argument("--chunk", type=int, default=0)
+    p.add_argument("--e2e-steps", type=int, default=4)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def make_schedule(mod, topo, n):
+    if topo == "one_peer_exponential":
+        return mod.make_one_peer_exponential(n)
+    if topo == "one_peer_ring":
+        return mod.make_one_peer_ring(n)
+    if topo == "static_exponential":
+        return mod.make_static_exponential(n)
+    return mod.make_aer(n, 2)
+
+
+def hyper(algo):
+    if algo == "dadam":
+        return dict(alpha=2e-3, beta1=0.974, beta2=0.999, eps=1e-8, s=1)
+    return dict(alpha=8e-4, beta1=0.9, beta2=0.999, eps=1e-8, s=4)
+
+
+def config_block(a, world, nodes):
+    return {
+        "workload": (f"BASELINE configs[1]/[4]: {a.topology.replace('_', ' ')} gossip, "
+                     f"{a.nodes_per_gpu} simulated nodes per B200 ({nodes} nodes), "
+                     f"{a.d:,}-param fp32 bucket per node, {a.algo}"),
+        "nodes": nodes, "nodes_per_gpu": a.nodes_per_gpu, "params_per_node": a.d,
+        "topology": a.topology, "algo": a.algo, "seed": SEED,
+        "parallelism": f"gossip over {world} GPU(s), nodes block-partitioned, NCCL send/recv over NVLink",
+        "l2": "no flush needed: every step streams >= 28 GB per GPU, > 126 MB L2",
+        "inputs": "synthetic StreamRng buckets (x0 ConsensusInit, g Minibatch@t=1 held fixed across timed steps)",
+    }
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]) * 1e9, "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650e9, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def read_traffic(key):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.rows, self.proc, self.th = [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        loaded = [float(r[1]) for r in self.rows if len(r) >= 9 and r[3].isdigit() and int(r[3]) > 0]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(loaded or sm) if (loaded or sm) else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def step_roofline(sched, world, d, steps_t, hbm_bw, per_update=HBM_PER_UPDATE):
+    """SURVEY.md 8(d) per-GPU step bound, summed over the timed rounds:
+    max over GPUs of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL)."""
+    import paper_2410_11998_b200 as dg
+    n = sched.workers()
+    total = 0.0
+    cache = {}
+    for t in steps_t:
+        r = (t - 1) % sched.period() + 1
+        if r not in cache:
+            worst = 0.0
+            for g in range(world):
+                sends, recvs = dg.plan_exchange(sched, world, g, r)
+                nl = sum(1 for i in range(n) if i * world // n == g)
+                t_hbm = d * (per_update * nl + HBM_PER_REMOTE * len(recvs)) / hbm_bw
+                t_nvl = 4.0 * d * max(len(recvs), len(sends)) / NVL_MEASURED
+                worst = max(worst, t_hbm, t_nvl)
+            cache[r] = worst
+        total += cache[r]
+    return total
+
+
+# ------------------------------------------------------------------------- CPU legs
+def cpu_reference_run(a, nodes_sample, d_sample, steps, threads):
+    """The reference CPU path (oracle/_ref: reference vec.cpp + parallel_for) on a
+    bounded sample; returns (updates/s, kind, note)."""
+    import numpy as np
+    from oracle import pyoracle as O
+    h = hyper(a.algo)
+    cfg = O.OptimizerConfig(**h)
+    algo = O.DADAM if a.algo == "dadam" else O.ACCUM
+    s = {"one_peer_exponential": O.make_one_peer_exponential, "one_peer_ring": O.make_one_peer_ring,
+         "static_exponential": O.make_static_exponential}.get(a.topology, lambda n: O.make_aer(n, 2))(nodes_sample)
+    st = O.init_state(nodes_sample, d_sample, SEED, True, np.float64, algo)
+    g = np.stack([O.fill_f32(SEED, O.MINIBATCH, i, 1, d_sample) for i in range(nodes_sample)]).astype(np.float64)
+    T = 4 * (steps + 1)
+    if O.ref_available():
+        el = O.ref_run(s, algo, cfg, SEED, st, 1, steps, T, threads, g_fixed=g)
+        kind = "reference"
+        note = ("oracle/_ref: the reference's proj/src/vec.cpp + rng.cpp + parallel.hpp compiled from "
+                "/root/reference, step composed per SPEC.md:272-280 (upstream ships no step code)")
+    else:
+        import ctypes as C
+        L = O.lib()
+        xprev = np.empty_like(st["x"])
+        c = cfg.c()
+        t0 = time.perf_counter()
+        for t in range(1, steps + 1):
+            rc = L.or_step_all_f64(s.handle, algo, C.byref(c), d_sample, t, T, threads, g.reshape(-1),
+                                   st["x"].reshape(-1), xprev.reshape(-1), st["m"].reshape(-1),
+                                   st["v"].reshape(-1), None)
+            assert rc == 0
+        el = time.perf_counter() - t0
+        kind = "port"
+        note = "oracle/oracle.cpp fp64 restatement (reference build absent)"
+    return nodes_sample * d_sample * steps / el, kind, note, el
+
+
+def cpu_baseline(a, budget_s):
+    import numpy as np  # noqa: F401
+    threads = os.cpu_count() or 1
+    nodes_sample, d_sample = 8, 1 << 21
+    # calibrate: 2 steps, then size the run to ~budget_s
+    rate, _, _, el = cpu_reference_run(a, nodes_sample, d_sample, 2, threads)
+    steps = max(3, int(budget_s * rate / (nodes_sample * d_sample)))
+    rate, kind, note, el = cpu_reference_run(a, nodes_sample, d_sample, steps, threads)
+    return {"value": rate, "unit": UNIT, "cores": min(threads, nodes_sample), "host_threads": threads,
+            "kind": kind,
+            "sample": (f"{nodes_sample} nodes x {d_sample:,} params (fp64), {steps} steps of the same "
+                       f"topology/algorithm, g held fixed; {el:.1f} s wall; OpenMP over nodes "
+                       f"(parallel.hpp:13-23 caps useful threads at the node count); {note}")}
+
+
+# ------------------------------------------------------------------------- reference arm
+def run_reference(a):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    nodes = a.nodes_per_gpu * world
+    threads = os.cpu_count() or 1
+    nodes_sample, d_sample = 8, 1 << 21
+    rate, kind, note, el = cpu_reference_run(a, nodes_sample, d_sample, a.warmup + a.steps, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1e3 * nodes_sample * d_sample / rate,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_block(a, world, nodes),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": min(threads, nodes_sample), "kind": kind,
+                         "sample": f"{nodes_sample} nodes x {d_sample:,} params per step (bounded sample of "
+                                   f"the workload), {a.warmup + a.steps} steps, {el:.1f} s; {note}"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------- our arm
+def run_ours(a):
+    import numpy as np
+    import torch
+    import paper_2410_11998_b200 as dg
+
+    rank, local, world = dist_env()
+    if world != a.gpus:
+        a.gpus = world
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    nodes = a.nodes_per_gpu * world
+    sched = make_schedule(dg, a.topology, nodes)
+    algo = dg.DADAM if a.algo == "dadam" else dg.ACCUM
+    h = hyper(a.algo)
+    total_t = a.warmup + a.steps + a.e2e_steps + 8
+    total_t += (-total_t) % 4
+    nccl_id = None
+    if world > 1:
+        obj = [dg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    eng = dg.Engine(sched, a.d, dg.OptimizerConfig(**h), algo=algo, total_steps=total_t, world_size=world,
+                    rank=rank, device=local, nccl_id=nccl_id, chunk=a.chunk)
+    eng.fill_synthetic(dg.X, SEED, dg.Stream.CONSENSUS_INIT, True, 0)
+    eng.fill_synthetic(dg.G, SEED, dg.Stream.MINIBATCH, True, 1)
+    eng.sync()
+    comp_ptr, _ = eng.streams()
+    comp = torch.cuda.ExternalStream(comp_ptr)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t = 0
+    for _ in range(a.warmup):
+        t += 1
+        eng.step(t)
+    eng.sync()
+
+    clocks = ClockSampler()
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.3)
+    # ---- timed region: K steps, CUDA events on the engine's compute stream
+    eng.set_timing(False)
+    eng.set_timing(True)
+    launches0 = eng.stats()["kernel_launches"]
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(comp)
+    timed_t = []
+    for _ in range(a.steps):
+        t += 1
+        timed_t.append(t)
+        eng.step(t)
+    ev1.record(comp)
+    eng.sync()
+    torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    st = eng.stats()
+    eng.set_timing(False)
+    clk = clocks.stop() if rank == 0 else None
+    ms_max = max_over_ranks(ms)
+    launches = st["kernel_launches"] - launches0
+    value = nodes * a.d * a.steps / (ms_max / 1e3)
+
+    # ---- roofline of the dominant kernel (fused gossip+Adam), live CUDA events
+    hbm_bw, peak_src = read_peaks()
+    kern_s = st["kernel_ms"] / 1e3
+    achieved = st["timed_hbm_bytes"] / kern_s if kern_s > 0 else 0.0
+    per_launch = st["timed_hbm_bytes"] / max(1, st["timed_launches"])
+    roof_step_s = step_roofline(sched, world, a.d, timed_t, hbm_bw)
+
+    # ---- end to end through the public API: pinned host g -> H2D each step, step, D2H status
+    e2e = None
+    if not a.no_e2e and a.e2e_steps > 0:
+        nl = eng.local_nodes
+        host = torch.empty((nl, a.d), dtype=torch.float32, pin_memory=True)
+        for i in range(nl):
+            host[i].copy_(torch.from_numpy(eng.download(i, dg.G)))
+        barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            t += 1
+            for i in range(nl):
+                eng.upload_ptr(i, dg.G, host[i].data_ptr(), a.d)
+            eng.step(t)
+            eng.sync()            # D2H read of the step's status (divergence flag, 4 B)
+        w1 = time.perf_counter()
+        e2e_s = max_over_ranks(w1 - w0)
+        e2e = {"value": nodes * a.d * a.e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": 4 * nl * a.d * world, "d2h_bytes_per_step": 4 * world,
+               "steps": a.e2e_steps,
+               "note": "pinned host gradients copied H2D every step (PCIe-bound), device-resident x/m/v"}
+        del host
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(a, a.cpu_seconds)
+
+    if rank == 0:
+        key = f"{a.topology}/{a.algo}/n{nodes}/g{world}/d{a.d}"
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_block(a, world, nodes),
+            "roofline": {"bound": "hbm", "achieved": achieved / 1e9, "peak": hbm_bw / 1e9, "unit": "GB/s",
+                         "frac": achieved / hbm_bw, "traffic": read_traffic(key),
+                         "algorithmic_bytes_per_launch": per_launch,
+                         "bytes_per_param_update": HBM_PER_UPDATE,
+                         "kernel_ms_per_launch": st["kernel_ms"] / max(1, st["timed_launches"]),
+                         "kernel_share_of_step": st["kernel_ms"] / ms if ms > 0 else None,
+                         "peak_source": peak_src, "kernel": "gossip_adam_fused"},
+            "step_roofline": {"bound_ms_per_step": 1e3 * roof_step_s / a.steps,
+                              "frac": (roof_step_s * 1e3) / ms_max,
+                              "model": "SURVEY.md 8(d): max over GPUs of max(HBM bytes/BW_HBM, NVLink bytes/770 GB/s)"},
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
+            "nvlink_bytes_sent_per_step": st["bytes_sent"] / max(1, st["steps"]),
+            "nccl_version": st["nccl_version"],
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()
