@@ -170,7 +170,9 @@ typedef struct dg_engine_stats {
 /* ncclGetUniqueId (call on rank 0, broadcast the 128 bytes to all ranks) */
 int dg_nccl_unique_id(void* out128);
 int dg_engine_create(const dg_engine_config* cfg, dg_engine** out);
-/* Borrowed device pointer of buffer `which` of resident node `local_node`. */
+/* Borrowed device pointer of buffer `which` of resident node `local_node`.
+ * Valid until the next dg_engine_step: rounds with large mixing components
+ * keep x double-buffered, so the DG_BUF_X pointer can alternate between steps. */
 int dg_engine_buffer(dg_engine* e, int local_node, int which, float** dev_ptr);
 /* Host <-> device copies of a node's buffer slice, ordered on the compute
  * stream.  upload is asynchronous (host memory must stay valid until the next

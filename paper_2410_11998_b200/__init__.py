@@ -31,7 +31,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "libdg.so")
+# DG_LIB overrides the library path (kernel-variant sweeps, scripts/sweep.py).
+_LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg.so")
 
 DADAM, ACCUM = 0, 1
 X, G, M, V, ACC = 0, 1, 2, 3, 4

@@ -82,11 +82,30 @@ struct RoundPlan {
   int src[kMaxLocal][kMaxDeg] = {};
   double w[kMaxLocal][kMaxDeg] = {};  // w_ij (the kernel mixes in fp64, rounds once)
   int max_deg = 0;
+  // mixing components: connected pieces of the round's mixing graph restricted
+  // to this GPU (one kernel grid row each)
+  struct Component {
+    std::vector<int> members;            // resident node indices, ascending
+    std::vector<int> srcs;               // distinct sources, ascending global id:
+                                         //   >= 0 resident node index, < 0 recv slot -(r+1)
+    std::vector<std::vector<double>> w;  // [member][source] weight, 0 = not a neighbour
+  };
+  std::vector<Component> comps;
+  int comp_size = 1;  // NC: power of two >= largest member count (comps * NC <= 16)
+  int src_bound = 2;  // NS: power of two >= largest source count, >= NC
+  // x double-buffered for this round: every resident node is its own
+  // component reading x^(t-1) from the current x buffer and writing x^(t) to
+  // the other one (large mixing components; see make_pingpong)
+  bool pingpong = false;
   // exchange (ordered by (peer, node))
   std::vector<int> send_peer, send_node;  // send_node: global id of a resident node
   std::vector<int> recv_peer, recv_node;  // recv slot r holds recv_node[r]
 };
 
 RoundPlan build_round_plan(const dg_schedule& s, int world, int rank, long round);
+// Re-express a round plan as one single-member component per resident node
+// (sources = that node's neighbours, ascending global id) for the
+// double-buffered x path.
+void make_pingpong(RoundPlan& p, int first_node);
 
 }  // namespace dg

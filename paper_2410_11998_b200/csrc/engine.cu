@@ -11,8 +11,10 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <string>
 
 #include "dg_internal.hpp"
 #include "kernels.cuh"
@@ -123,65 +125,120 @@ int* semantic_flag() {
 }
 
 // ------------------------------------------------------------------ fused launch table
-using LaunchFn = void (*)(const void* args, unsigned grid, cudaStream_t st);
+// One entry per (component size NC, degree bound DEG, algorithm, fold).  Each
+// entry sizes its grid from the occupancy API so that exactly one wave of
+// CTAs is resident (grid-stride loop inside), split across the components.
+using LaunchFn = void (*)(const void* args, long long cols, int n_comp, cudaStream_t st);
 
-template <int NL, int DEG, int ALGO, bool FOLD>
-void launch_fused(const void* args, unsigned grid, cudaStream_t st) {
-  gossip_adam_fused<NL, DEG, ALGO, FOLD>
-      <<<grid, 256, 0, st>>>(*static_cast<const FusedArgs<NL, DEG>*>(args));
+double grid_waves() {  // DG_WAVES: resident-wave multiplier (tuning knob, default 1)
+  static const double w = [] {
+    const char* e = std::getenv("DG_WAVES");
+    return e ? std::max(0.05, std::atof(e)) : 1.0;
+  }();
+  return w;
 }
 
-template <int NL, int DEG>
+int coop_min_nc() {  // DG_COOP_MIN_NC: smallest component size using the cooperative kernel
+  static const int v = [] {
+    const char* e = std::getenv("DG_COOP_MIN_NC");
+    return e ? std::atoi(e) : 4;
+  }();
+  return v;
+}
+
+template <int NC, int NS, int ALGO, bool FOLD>
+void launch_coop(const void* args, long long cols, int n_comp, cudaStream_t st) {
+  auto kern = gossip_adam_coop<NC, NS, ALGO, FOLD>;
+  constexpr int threads = CoopShape<NC, NS>::threads;
+  static const int occ = [&] {
+    int o = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, 0), "occupancy");
+    return std::max(1, o);
+  }();
+  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * current_sms()));
+  const long long per_comp = std::max(1LL, resident / n_comp);
+  const long long need = (cols * NC + threads - 1) / threads;
+  const dim3 grid(unsigned(std::max(1LL, std::min(per_comp, need))), unsigned(n_comp));
+  kern<<<grid, threads, 0, st>>>(*static_cast<const FusedArgs<NC, NS>*>(args));
+}
+
+template <int NC, int NS, int ALGO, bool FOLD>
+void launch_fused(const void* args, long long cols, int n_comp, cudaStream_t st) {
+  if constexpr (NC >= 2) {
+    if (NC >= coop_min_nc()) return launch_coop<NC, NS, ALGO, FOLD>(args, cols, n_comp, st);
+  }
+  auto kern = gossip_adam_fused<NC, NS, ALGO, FOLD>;
+  constexpr int threads = LaunchShape<NC, NS>::threads;
+  static const int occ = [&] {
+    int o = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, 0), "occupancy");
+    return std::max(1, o);
+  }();
+  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * current_sms()));
+  const long long per_comp = std::max(1LL, resident / n_comp);
+  const long long need = (cols + threads - 1) / threads;
+  const dim3 grid(unsigned(std::max(1LL, std::min(per_comp, need))), unsigned(n_comp));
+  kern<<<grid, threads, 0, st>>>(*static_cast<const FusedArgs<NC, NS>*>(args));
+}
+
+template <int NC, int NS>
 LaunchFn pick_algo(int algo, bool fold) {
-  if (algo == DG_ALGO_DADAM) return launch_fused<NL, DEG, 0, false>;
-  return fold ? launch_fused<NL, DEG, 1, true> : launch_fused<NL, DEG, 1, false>;
+  if (algo == DG_ALGO_DADAM) return launch_fused<NC, NS, 0, false>;
+  return fold ? launch_fused<NC, NS, 1, true> : launch_fused<NC, NS, 1, false>;
 }
-template <int NL>
-LaunchFn pick_deg(int deg, int algo, bool fold) {
-  if (deg <= 2) return pick_algo<NL, 2>(algo, fold);
-  if (deg <= 4) return pick_algo<NL, 4>(algo, fold);
-  if (deg <= 8) return pick_algo<NL, 8>(algo, fold);
-  return pick_algo<NL, 16>(algo, fold);
+template <int NC>
+LaunchFn pick_ns(int ns, int algo, bool fold) {
+  // instantiated only for NS >= NC
+  if (ns <= 2 && NC <= 2) return pick_algo<NC, (NC <= 2 ? 2 : NC)>(algo, fold);
+  if (ns <= 4 && NC <= 4) return pick_algo<NC, (NC <= 4 ? 4 : NC)>(algo, fold);
+  if (ns <= 8 && NC <= 8) return pick_algo<NC, (NC <= 8 ? 8 : NC)>(algo, fold);
+  if (ns <= 16) return pick_algo<NC, 16>(algo, fold);
+  return pick_algo<NC, 32>(algo, fold);
 }
-int round_pow2(int x) {
-  int p = 1;
-  while (p < x) p <<= 1;
-  return p;
-}
-int round_deg(int d) { return d <= 2 ? 2 : d <= 4 ? 4 : d <= 8 ? 8 : 16; }
-LaunchFn pick(int nl, int deg, int algo, bool fold) {
-  switch (round_pow2(nl)) {
-    case 1: return pick_deg<1>(deg, algo, fold);
-    case 2: return pick_deg<2>(deg, algo, fold);
-    case 4: return pick_deg<4>(deg, algo, fold);
-    case 8: return pick_deg<8>(deg, algo, fold);
-    default: return pick_deg<16>(deg, algo, fold);
+LaunchFn pick(int nc, int ns, int algo, bool fold) {
+  switch (nc) {
+    case 1: return pick_ns<1>(ns, algo, fold);
+    case 2: return pick_ns<2>(ns, algo, fold);
+    case 4: return pick_ns<4>(ns, algo, fold);
+    case 8: return pick_ns<8>(ns, algo, fold);
+    default: return pick_ns<16>(ns, algo, fold);
   }
 }
 
-// Fills a FusedArgs<NL,DEG> image in a byte buffer (layout computed by the template).
-template <int NL, int DEG>
-void fill_args_t(std::vector<unsigned char>& buf, const RoundPlan& p, const float* const* local_x,
-                 const float* const* slot, float* const* x, const float* const* g, float* const* m,
-                 float* const* v, float* const* b, size_t off, size_t len, const DevScalars& s,
-                 int t, int* flag) {
-  buf.assign(sizeof(FusedArgs<NL, DEG>), 0);
-  auto* a = reinterpret_cast<FusedArgs<NL, DEG>*>(buf.data());
-  for (int i = 0; i < NL; ++i) {
-    a->deg[i] = i < p.n_local ? p.deg[i] : 0;
-    for (int k = 0; k < DEG; ++k) {
-      if (i < p.n_local && k < p.deg[i]) {
-        const int sidx = p.src[i][k];
-        a->src[i][k] = sidx < p.n_local ? local_x[sidx] + off : slot[sidx - p.n_local];
-        a->w[i][k] = p.w[i][k];
-      }
+// Builds the FusedArgs<NC,NS> image of one launch in a byte buffer.
+struct Buffers {
+  const float* const* slot;  // recv slot base per remote source (already at chunk start)
+  float* const* x;           // x^(t-1) (mixing sources)
+  float* const* xout;        // where x^(t) goes (== x in place, the other buffer when ping-pong)
+  const float* const* g;
+  float* const* m;
+  float* const* v;
+  float* const* b;  // null for DAdam
+};
+template <int NC, int NS>
+void fill_args_t(std::vector<unsigned char>& buf, const RoundPlan& p, const Buffers& bf, size_t off,
+                 size_t len, const DevScalars& s, int t, int* flag) {
+  using A = FusedArgs<NC, NS>;
+  buf.assign(sizeof(A), 0);
+  auto* a = reinterpret_cast<A*>(buf.data());
+  if (int(p.comps.size()) > A::CMAX) config_error("plan: too many mixing components");
+  for (size_t c = 0; c < p.comps.size(); ++c) {
+    const auto& cp = p.comps[c];
+    if (int(cp.members.size()) > NC || int(cp.srcs.size()) > NS) config_error("plan: component too large");
+    a->nm[c] = int(cp.members.size());
+    a->ns[c] = int(cp.srcs.size());
+    for (size_t k = 0; k < cp.srcs.size(); ++k) {
+      const int code = cp.srcs[k];
+      a->src[c][k] = code >= 0 ? bf.x[code] + off : bf.slot[-code - 1];
     }
-    if (i < p.n_local) {
-      a->x[i] = x[i] + off;
-      a->g[i] = g[i] + off;
-      a->m[i] = m[i] + off;
-      a->v[i] = v[i] + off;
-      a->b[i] = b ? b[i] + off : nullptr;
+    for (size_t j = 0; j < cp.members.size(); ++j) {
+      const int li = cp.members[j];
+      for (size_t k = 0; k < cp.srcs.size(); ++k) a->w[c][j][k] = cp.w[j][k];
+      a->x[c][j] = bf.xout[li] + off;
+      a->g[c][j] = bf.g[li] + off;
+      a->m[c][j] = bf.m[li] + off;
+      a->v[c][j] = bf.v[li] + off;
+      a->b[c][j] = bf.b ? bf.b[li] + off : nullptr;
     }
   }
   a->s = s;
@@ -189,35 +246,151 @@ void fill_args_t(std::vector<unsigned char>& buf, const RoundPlan& p, const floa
   a->t = t;
   a->div_flag = flag;
 }
-template <int NL>
-void fill_deg(int deg, std::vector<unsigned char>& buf, const RoundPlan& p, const float* const* lx,
-              const float* const* slot, float* const* x, const float* const* g, float* const* m,
-              float* const* v, float* const* b, size_t off, size_t len, const DevScalars& s, int t,
-              int* flag) {
-  switch (round_deg(deg)) {
-    case 2: return fill_args_t<NL, 2>(buf, p, lx, slot, x, g, m, v, b, off, len, s, t, flag);
-    case 4: return fill_args_t<NL, 4>(buf, p, lx, slot, x, g, m, v, b, off, len, s, t, flag);
-    case 8: return fill_args_t<NL, 8>(buf, p, lx, slot, x, g, m, v, b, off, len, s, t, flag);
-    default: return fill_args_t<NL, 16>(buf, p, lx, slot, x, g, m, v, b, off, len, s, t, flag);
+template <int NC>
+void fill_ns(std::vector<unsigned char>& buf, const RoundPlan& p, const Buffers& bf, size_t off,
+             size_t len, const DevScalars& s, int t, int* flag) {
+  const int ns = p.src_bound;
+  if (ns <= 2 && NC <= 2) return fill_args_t<NC, (NC <= 2 ? 2 : NC)>(buf, p, bf, off, len, s, t, flag);
+  if (ns <= 4 && NC <= 4) return fill_args_t<NC, (NC <= 4 ? 4 : NC)>(buf, p, bf, off, len, s, t, flag);
+  if (ns <= 8 && NC <= 8) return fill_args_t<NC, (NC <= 8 ? 8 : NC)>(buf, p, bf, off, len, s, t, flag);
+  if (ns <= 16) return fill_args_t<NC, 16>(buf, p, bf, off, len, s, t, flag);
+  return fill_args_t<NC, 32>(buf, p, bf, off, len, s, t, flag);
+}
+void fill_args(std::vector<unsigned char>& buf, const RoundPlan& p, const Buffers& bf, size_t off,
+               size_t len, const DevScalars& s, int t, int* flag) {
+  switch (p.comp_size) {
+    case 1: return fill_ns<1>(buf, p, bf, off, len, s, t, flag);
+    case 2: return fill_ns<2>(buf, p, bf, off, len, s, t, flag);
+    case 4: return fill_ns<4>(buf, p, bf, off, len, s, t, flag);
+    case 8: return fill_ns<8>(buf, p, bf, off, len, s, t, flag);
+    default: return fill_ns<16>(buf, p, bf, off, len, s, t, flag);
   }
 }
-void fill_args(std::vector<unsigned char>& buf, const RoundPlan& p, const float* const* lx,
-               const float* const* slot, float* const* x, const float* const* g, float* const* m,
-               float* const* v, float* const* b, size_t off, size_t len, const DevScalars& s,
-               int t, int* flag) {
-  switch (round_pow2(p.n_local)) {
-    case 1: return fill_deg<1>(p.max_deg, buf, p, lx, slot, x, g, m, v, b, off, len, s, t, flag);
-    case 2: return fill_deg<2>(p.max_deg, buf, p, lx, slot, x, g, m, v, b, off, len, s, t, flag);
-    case 4: return fill_deg<4>(p.max_deg, buf, p, lx, slot, x, g, m, v, b, off, len, s, t, flag);
-    case 8: return fill_deg<8>(p.max_deg, buf, p, lx, slot, x, g, m, v, b, off, len, s, t, flag);
-    default: return fill_deg<16>(p.max_deg, buf, p, lx, slot, x, g, m, v, b, off, len, s, t, flag);
+
+// ------------------------------------------------------------------ TMA-staged launch
+int tma_mode() {  // DG_TMA: 0 never (default), 1 components of >= 4 members, 2 always
+  static const int v = [] {
+    const char* e = std::getenv("DG_TMA");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+bool use_tma(const RoundPlan& p) {
+  const int m = tma_mode();
+  return m == 2 || (m == 1 && p.comp_size >= 4);
+}
+
+bool staged_bulk() {  // DG_STAGE_COPY: "tma" (bulk copies, default) or "async" (cp.async)
+  static const bool v = [] {
+    const char* e = std::getenv("DG_STAGE_COPY");
+    return !(e && std::string(e) == "async");
+  }();
+  return v;
+}
+
+template <int ALGO, bool FOLD, bool BULK, int NS>
+void launch_tma_b(const TmaArgs& a, size_t smem, long long units, cudaStream_t st) {
+  auto kern = gossip_adam_tma<ALGO, FOLD, BULK, NS>;
+  static bool configured = false;
+  if (!configured) {
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+               "tma smem attribute");
+    configured = true;
   }
+  int occ = 0;
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTmaThreads, smem), "tma occupancy");
+  const long long resident = std::max(1LL, (long long)std::max(1, occ) * current_sms());
+  const unsigned grid = unsigned(std::max(1LL, std::min(units, resident)));
+  kern<<<grid, kTmaThreads, smem, st>>>(a);
+}
+template <int ALGO, bool FOLD, int NS>
+void launch_tma_n(const TmaArgs& a, size_t smem, long long units, cudaStream_t st) {
+  if (staged_bulk())
+    launch_tma_b<ALGO, FOLD, true, NS>(a, smem, units, st);
+  else
+    launch_tma_b<ALGO, FOLD, false, NS>(a, smem, units, st);
+}
+template <int ALGO, bool FOLD>
+void launch_tma_t(const TmaArgs& a, int ns_max, size_t smem, long long units, cudaStream_t st) {
+  if (ns_max <= 2) return launch_tma_n<ALGO, FOLD, 2>(a, smem, units, st);
+  if (ns_max <= 4) return launch_tma_n<ALGO, FOLD, 4>(a, smem, units, st);
+  if (ns_max <= 8) return launch_tma_n<ALGO, FOLD, 8>(a, smem, units, st);
+  if (ns_max <= 16) return launch_tma_n<ALGO, FOLD, 16>(a, smem, units, st);
+  return launch_tma_n<ALGO, FOLD, 32>(a, smem, units, st);
+}
+
+void launch_tma(const RoundPlan& p, const Buffers& bf, int algo, bool fold, size_t off, size_t len,
+                const DevScalars& s, int t, int* flag, cudaStream_t st) {
+  static TmaArgs a;  // large POD; one engine call at a time per thread of use
+  std::memset(&a, 0, sizeof(a));
+  const int K = algo == DG_ALGO_ACCUM ? 4 : 3;
+  a.n_comp = int(p.comps.size());
+  int row = 0, rows_max = 0, srow = 0;
+  for (size_t c = 0; c < p.comps.size(); ++c) {
+    const auto& cp = p.comps[c];
+    if (int(cp.srcs.size()) > kTmaMaxSrc) config_error("tma: too many sources in a component");
+    a.nm[c] = int(cp.members.size());
+    a.ns[c] = int(cp.srcs.size());
+    a.row0[c] = row;
+    a.srow0[c] = srow;
+    const int rows = a.ns[c] + a.nm[c] * K;
+    if (srow + rows > kTmaMaxRows) config_error("tma: too many staged rows");
+    for (size_t k = 0; k < cp.srcs.size(); ++k) {
+      const int code = cp.srcs[k];
+      a.row_ptr[srow++] = code >= 0 ? bf.x[code] + off : bf.slot[-code - 1];
+    }
+    for (size_t j = 0; j < cp.members.size(); ++j, ++row) {
+      const int li = cp.members[j];
+      a.row_node[row] = li;
+      for (size_t k = 0; k < cp.srcs.size(); ++k) a.w[row][k] = cp.w[j][k];
+      a.row_ptr[srow++] = bf.g[li] + off;
+      a.row_ptr[srow++] = bf.m[li] + off;
+      a.row_ptr[srow++] = bf.v[li] + off;
+      if (K == 4) a.row_ptr[srow++] = bf.b[li] + off;
+    }
+    rows_max = std::max(rows_max, rows);
+  }
+  for (int i = 0; i < p.n_local; ++i) {
+    a.xb[i] = bf.xout[i] + off;
+    a.mb[i] = bf.m[i] + off;
+    a.vb[i] = bf.v[i] + off;
+    a.bb[i] = bf.b ? bf.b[i] + off : nullptr;
+  }
+  a.s = s;
+  a.n = (long long)len;
+  // tile: as large as the stage budget allows, with members x float4 columns a
+  // multiple of the CTA size so every thread gets the same number of items
+  int nm_max = 1, ns_max = 2;
+  for (int c = 0; c < a.n_comp; ++c) {
+    nm_max = std::max(nm_max, a.nm[c]);
+    ns_max = std::max(ns_max, a.ns[c]);
+  }
+  int cols = kTmaThreads / std::min(nm_max, kTmaThreads) / 32 * 32;  // float4 columns per thread round
+  cols = std::max(32, cols);
+  const int max_cols = DG_TMA_STAGE_BYTES / (16 * rows_max);
+  const int tile4 = max_cols >= cols ? max_cols / cols * cols : std::max(32, max_cols / 32 * 32);
+  a.tile = tile4 * 4;
+  a.rows_max = rows_max;
+  a.t = t;
+  a.div_flag = flag;
+  const size_t smem = 128 + size_t(DG_TMA_STAGES) * rows_max * a.tile * sizeof(float);
+  const long long units = ((long long)len + a.tile - 1) / a.tile * a.n_comp;
+  if (algo == DG_ALGO_DADAM)
+    launch_tma_t<0, false>(a, ns_max, smem, units, st);
+  else if (fold)
+    launch_tma_t<1, true>(a, ns_max, smem, units, st);
+  else
+    launch_tma_t<1, false>(a, ns_max, smem, units, st);
 }
 
 }  // namespace
 }  // namespace dg
 
 // ===================================================================== engine
+struct LaunchFnHolder {
+  dg::LaunchFn fn;
+};
+
 struct dg_engine {
   // configuration
   int N = 0, G = 1, rank = 0, device = 0, algo = 0, first = 0, NL = 0, P = 0;
@@ -249,7 +422,13 @@ struct dg_engine {
   long timed_launches = 0;
   void harvest_timing();
 
-  float* buf(int which, int local) const { return arena[which] + size_t(local) * d_pad; }
+  float* x_alt = nullptr;  // second x buffer (ping-pong rounds)
+  int xcur = 0;            // which x buffer holds the current x
+  float* buf(int which, int local) const {
+    const float* base = (which == DG_BUF_X && xcur) ? x_alt : arena[which];
+    return const_cast<float*>(base) + size_t(local) * d_pad;
+  }
+  float* x_other(int local) const { return (xcur ? arena[DG_BUF_X] : x_alt) + size_t(local) * d_pad; }
   void enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
                      const dg::DevScalars& s, bool fold, long t);
   void step(long t);
@@ -264,6 +443,7 @@ dg_engine::~dg_engine() {
   for (float* a : arena)
     if (a) cudaFree(a);
   if (slots) cudaFree(slots);
+  if (x_alt) cudaFree(x_alt);
   if (flag) cudaFree(flag);
   if (ev_begin) cudaEventDestroy(ev_begin);
   for (auto e : ev_slot_free)
@@ -279,11 +459,11 @@ dg_engine::~dg_engine() {
 
 void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
                               const dg::DevScalars& s, bool fold, long t) {
-  const float* lx[dg::kMaxLocal];
-  float *x[dg::kMaxLocal], *m[dg::kMaxLocal], *v[dg::kMaxLocal], *b[dg::kMaxLocal];
+  float *x[dg::kMaxLocal], *xo[dg::kMaxLocal], *m[dg::kMaxLocal], *v[dg::kMaxLocal], *b[dg::kMaxLocal];
   const float* g[dg::kMaxLocal];
   for (int i = 0; i < NL; ++i) {
-    lx[i] = x[i] = buf(DG_BUF_X, i);
+    x[i] = buf(DG_BUF_X, i);
+    xo[i] = p.pingpong ? x_other(i) : x[i];
     g[i] = buf(DG_BUF_G, i);
     m[i] = buf(DG_BUF_M, i);
     v[i] = buf(DG_BUF_V, i);
@@ -292,9 +472,13 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   const float* slot_ptr[dg::kMaxRemote];
   for (int r = 0; r < int(p.recv_node.size()); ++r)
     slot_ptr[r] = slots + (size_t(slot_set) * max_recv + r) * chunk;
-  dg::fill_args(argbuf, p, lx, slot_ptr, x, g, m, v, b, off, len, s, int(t), flag);
-  const auto fn = dg::pick(p.n_local, p.max_deg, algo, fold);
-  const unsigned grid = dg::grid_for((long long)(len + 3) / 4, blocks_per_sm);
+  const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr};
+  const bool tma = dg::use_tma(p);
+  LaunchFnHolder fnh{nullptr};
+  if (!tma) {
+    dg::fill_args(argbuf, p, bf, off, len, s, int(t), flag);
+    fnh.fn = dg::pick(p.comp_size, p.src_bound, algo, fold);
+  }
   const double per = algo == DG_ALGO_DADAM ? 28.0 : (fold ? 36.0 : 28.0);
   const double bytes = double(len) * (per * p.n_local + 4.0 * double(p.recv_node.size()));
   if (timing) {
@@ -307,7 +491,10 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
     }
     CU(cudaEventRecord(tev[tev_used].first, comp));
   }
-  fn(argbuf.data(), grid, comp);
+  if (tma)
+    dg::launch_tma(p, bf, algo, fold, off, len, s, int(t), flag, comp);
+  else
+    fnh.fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), comp);
   dg::cuda_check(cudaGetLastError(), "fused kernel launch");
   if (timing) {
     CU(cudaEventRecord(tev[tev_used].second, comp));
@@ -336,6 +523,7 @@ void dg_engine::step(long t) {
   ++steps;
   if (p.send_node.empty() && p.recv_node.empty()) {  // intra-GPU round: one launch
     enqueue_fused(p, 0, d, 0, s, fold, t);
+    if (p.pingpong) xcur ^= 1;
     return;
   }
   // comm stream starts after everything already queued on the compute stream
@@ -363,6 +551,7 @@ void dg_engine::step(long t) {
     enqueue_fused(p, off, len, set, s, fold, t);
     CU(cudaEventRecord(ev_slot_free[set], comp));
   }
+  if (p.pingpong) xcur ^= 1;
 }
 
 // ===================================================================== C ABI
@@ -412,6 +601,17 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       e->max_recv = std::max(e->max_recv, int(e->plans.back().recv_node.size()));
     }
     e->NL = e->plans[0].n_local;
+    // rounds with mixing components of >= DG_PINGPONG_MIN_NC members (default 4)
+    // run with x double-buffered (one lean gather per node instead of one
+    // thread carrying a whole component)
+    const char* ppenv = std::getenv("DG_PINGPONG_MIN_NC");
+    const int pp_min = ppenv ? std::atoi(ppenv) : 4;
+    bool any_pp = false;
+    for (auto& p : e->plans)
+      if (pp_min > 0 && p.comp_size >= pp_min) {
+        dg::make_pingpong(p, e->first);
+        any_pp = true;
+      }
     if (e->NL < 1) dg::config_error("engine_create: no resident nodes on this rank");
     CU(cudaSetDevice(c->device));
     int lo = 0, hi = 0;
@@ -426,6 +626,10 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     for (int k = 0; k < kinds; ++k) {
       CU(cudaMalloc(&e->arena[k], sizeof(float) * e->d_pad * e->NL));
       CU(cudaMemsetAsync(e->arena[k], 0, sizeof(float) * e->d_pad * e->NL, e->comp));
+    }
+    if (any_pp) {
+      CU(cudaMalloc(&e->x_alt, sizeof(float) * e->d_pad * e->NL));
+      CU(cudaMemsetAsync(e->x_alt, 0, sizeof(float) * e->d_pad * e->NL, e->comp));
     }
     if (e->max_recv) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
     CU(cudaMalloc(&e->flag, sizeof(int)));

@@ -8,6 +8,8 @@
 // are materialised only for validation and for dg_schedule_matrix.
 #include <algorithm>
 #include <cmath>
+#include <climits>
+#include <cstdint>
 #include <cstring>
 #include <numeric>
 
@@ -231,6 +233,71 @@ dg::RoundPlan dg::build_round_plan(const dg_schedule& s, int world, int rank, lo
       p.w[li][k] = rd.w[i][k];
     }
   }
+  // mixing components: union-find over resident-resident edges of the round
+  {
+    std::vector<int> par(p.n_local);
+    std::iota(par.begin(), par.end(), 0);
+    auto find = [&](int x) {
+      while (par[x] != x) x = par[x] = par[par[x]];
+      return x;
+    };
+    for (int li = 0; li < p.n_local; ++li)
+      for (int k = 0; k < p.deg[li]; ++k)
+        if (p.src[li][k] < p.n_local) par[find(li)] = find(p.src[li][k]);
+    std::vector<std::vector<int>> comps;
+    std::vector<int> comp_of(p.n_local, -1);
+    for (int li = 0; li < p.n_local; ++li) {  // ascending => components ordered by first node
+      const int r = find(li);
+      if (comp_of[r] < 0) {
+        comp_of[r] = int(comps.size());
+        comps.emplace_back();
+      }
+      comps[comp_of[r]].push_back(li);
+    }
+    size_t biggest = 0;
+    for (const auto& c : comps) biggest = std::max(biggest, c.size());
+    int cs = 1;
+    while (cs < int(biggest)) cs <<= 1;
+    if (int(comps.size()) * cs > kMaxLocal) {  // too much padding: one component of everything
+      std::vector<int> all(p.n_local);
+      std::iota(all.begin(), all.end(), 0);
+      comps = {all};
+      cs = 1;
+      while (cs < p.n_local) cs <<= 1;
+    }
+    p.comp_size = cs;
+    int nsb = 2;
+    for (const auto& members : comps) {
+      RoundPlan::Component c;
+      c.members = members;
+      std::vector<std::pair<int, int>> src;  // (global id, source code)
+      for (int li : members)
+        for (int k = 0; k < p.deg[li]; ++k) {
+          const int sidx = p.src[li][k];
+          const int code = sidx < p.n_local ? sidx : -(sidx - p.n_local + 1);
+          const int gid = sidx < p.n_local ? first + sidx : p.recv_node[sidx - p.n_local];
+          src.push_back({gid, code});
+        }
+      std::sort(src.begin(), src.end());
+      src.erase(std::unique(src.begin(), src.end()), src.end());
+      for (auto [gid, code] : src) c.srcs.push_back(code);
+      c.w.assign(members.size(), std::vector<double>(src.size(), 0.0));
+      for (size_t jm = 0; jm < members.size(); ++jm) {
+        const int li = members[jm];
+        for (int k = 0; k < p.deg[li]; ++k) {
+          const int sidx = p.src[li][k];
+          const int gid = sidx < p.n_local ? first + sidx : p.recv_node[sidx - p.n_local];
+          const size_t pos =
+              std::lower_bound(src.begin(), src.end(), std::make_pair(gid, INT32_MIN)) - src.begin();
+          c.w[jm][pos] = p.w[li][k];
+        }
+      }
+      while (nsb < int(src.size())) nsb <<= 1;
+      p.comps.push_back(std::move(c));
+    }
+    p.src_bound = std::max(nsb, cs);
+    if (p.src_bound > 32) config_error("plan: more than 32 distinct sources in one mixing component");
+  }
   // sends: resident node j goes to every other rank hosting a node that mixes j
   std::vector<std::pair<int, int>> sends;
   for (int i = 0; i < N; ++i) {
@@ -246,6 +313,32 @@ dg::RoundPlan dg::build_round_plan(const dg_schedule& s, int world, int rank, lo
     p.send_node.push_back(j);
   }
   return p;
+}
+
+void dg::make_pingpong(RoundPlan& p, int first) {
+  p.comps.clear();
+  p.comp_size = 1;
+  int nsb = 2;
+  for (int li = 0; li < p.n_local; ++li) {
+    RoundPlan::Component c;
+    c.members = {li};
+    std::vector<std::pair<int, int>> src;  // (global id, k)
+    for (int k = 0; k < p.deg[li]; ++k) {
+      const int sidx = p.src[li][k];
+      src.push_back({sidx < p.n_local ? first + sidx : p.recv_node[sidx - p.n_local], k});
+    }
+    std::sort(src.begin(), src.end());
+    c.w.assign(1, std::vector<double>());
+    for (auto [gid, k] : src) {
+      const int sidx = p.src[li][k];
+      c.srcs.push_back(sidx < p.n_local ? sidx : -(sidx - p.n_local + 1));
+      c.w[0].push_back(p.w[li][k]);
+    }
+    while (nsb < int(c.srcs.size())) nsb <<= 1;
+    p.comps.push_back(std::move(c));
+  }
+  p.src_bound = nsb;
+  p.pingpong = true;
 }
 
 // ================================================================== C ABI

@@ -1,0 +1,30 @@
+"""Every fused-kernel path (TMA-staged, cooperative, per-thread) must be
+bit-exact against the oracle's fp32 mirror for every topology; the path is
+chosen by env knobs read once per process, hence one subprocess per path."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PATHS = {"default": {},
+         "pingpong_all": {"DG_PINGPONG_MIN_NC": "1"},
+         "tma_all": {"DG_TMA": "2", "DG_PINGPONG_MIN_NC": "0"},
+         "tma_pingpong": {"DG_TMA": "2", "DG_PINGPONG_MIN_NC": "1"},
+         "per_thread_all": {"DG_TMA": "0", "DG_COOP_MIN_NC": "99", "DG_PINGPONG_MIN_NC": "0"},
+         "coop_all": {"DG_TMA": "0", "DG_COOP_MIN_NC": "2", "DG_PINGPONG_MIN_NC": "0"}}
+
+
+@pytest.mark.parametrize("path", sorted(PATHS))
+@pytest.mark.parametrize("d", [5003, 300_001])
+def test_kernel_path_bit_exact(path, d):
+    env = {**os.environ, **PATHS[path]}
+    p = subprocess.run([sys.executable, os.path.join(HERE, "engine_parity_main.py"), str(d)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
