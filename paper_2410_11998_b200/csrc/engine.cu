@@ -128,7 +128,7 @@ int* semantic_flag() {
 // One entry per (component size NC, degree bound DEG, algorithm, fold).  Each
 // entry sizes its grid from the occupancy API so that exactly one wave of
 // CTAs is resident (grid-stride loop inside), split across the components.
-using LaunchFn = void (*)(const void* args, long long cols, int n_comp, cudaStream_t st);
+using LaunchFn = void (*)(const void* args, long long cols, int n_comp, int sms, cudaStream_t st);
 
 double grid_waves() {  // DG_WAVES: resident-wave multiplier (tuning knob, default 1)
   static const double w = [] {
@@ -147,7 +147,7 @@ int coop_min_nc() {  // DG_COOP_MIN_NC: smallest component size using the cooper
 }
 
 template <int NC, int NS, int ALGO, bool FOLD>
-void launch_coop(const void* args, long long cols, int n_comp, cudaStream_t st) {
+void launch_coop(const void* args, long long cols, int n_comp, int sms, cudaStream_t st) {
   auto kern = gossip_adam_coop<NC, NS, ALGO, FOLD>;
   constexpr int threads = CoopShape<NC, NS>::threads;
   static const int occ = [&] {
@@ -155,7 +155,7 @@ void launch_coop(const void* args, long long cols, int n_comp, cudaStream_t st) 
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, 0), "occupancy");
     return std::max(1, o);
   }();
-  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * current_sms()));
+  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * sms));
   const long long per_comp = std::max(1LL, resident / n_comp);
   const long long need = (cols * NC + threads - 1) / threads;
   const dim3 grid(unsigned(std::max(1LL, std::min(per_comp, need))), unsigned(n_comp));
@@ -163,9 +163,9 @@ void launch_coop(const void* args, long long cols, int n_comp, cudaStream_t st) 
 }
 
 template <int NC, int NS, int ALGO, bool FOLD>
-void launch_fused(const void* args, long long cols, int n_comp, cudaStream_t st) {
+void launch_fused(const void* args, long long cols, int n_comp, int sms, cudaStream_t st) {
   if constexpr (NC >= 2) {
-    if (NC >= coop_min_nc()) return launch_coop<NC, NS, ALGO, FOLD>(args, cols, n_comp, st);
+    if (NC >= coop_min_nc()) return launch_coop<NC, NS, ALGO, FOLD>(args, cols, n_comp, sms, st);
   }
   auto kern = gossip_adam_fused<NC, NS, ALGO, FOLD>;
   constexpr int threads = LaunchShape<NC, NS>::threads;
@@ -174,7 +174,7 @@ void launch_fused(const void* args, long long cols, int n_comp, cudaStream_t st)
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, 0), "occupancy");
     return std::max(1, o);
   }();
-  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * current_sms()));
+  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * sms));
   const long long per_comp = std::max(1LL, resident / n_comp);
   const long long need = (cols + threads - 1) / threads;
   const dim3 grid(unsigned(std::max(1LL, std::min(per_comp, need))), unsigned(n_comp));
@@ -429,6 +429,14 @@ struct dg_engine {
     return const_cast<float*>(base) + size_t(local) * d_pad;
   }
   float* x_other(int local) const { return (xcur ? arena[DG_BUF_X] : x_alt) + size_t(local) * d_pad; }
+  // SMs the fused kernel may fill: all of them in intra-GPU rounds; in exchange
+  // rounds DG_RESERVE_SMS (default 0) are left to NCCL's kernels
+  int sm_total = 0, reserve_sms = 0;
+  bool diag_skip_kernel = false;  // DG_DIAG_SKIP_KERNEL: exchange only (diagnostics; wrong results)
+  int sms_for(const dg::RoundPlan& p) const {
+    const bool comm = !(p.send_node.empty() && p.recv_node.empty());
+    return std::max(1, comm ? sm_total - reserve_sms : sm_total);
+  }
   void enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
                      const dg::DevScalars& s, bool fold, long t);
   void step(long t);
@@ -494,7 +502,7 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   if (tma)
     dg::launch_tma(p, bf, algo, fold, off, len, s, int(t), flag, comp);
   else
-    fnh.fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), comp);
+    fnh.fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), sms_for(p), comp);
   dg::cuda_check(cudaGetLastError(), "fused kernel launch");
   if (timing) {
     CU(cudaEventRecord(tev[tev_used].second, comp));
@@ -548,7 +556,7 @@ void dg_engine::step(long t) {
     // fused kernel on chunk k once its neighbour buckets have landed (and the
     // sends of the in-place x chunk have drained)
     CU(cudaStreamWaitEvent(comp, ev_recv[k], 0));
-    enqueue_fused(p, off, len, set, s, fold, t);
+    if (!diag_skip_kernel) enqueue_fused(p, off, len, set, s, fold, t);
     CU(cudaEventRecord(ev_slot_free[set], comp));
   }
   if (p.pingpong) xcur ^= 1;
@@ -614,6 +622,9 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       }
     if (e->NL < 1) dg::config_error("engine_create: no resident nodes on this rank");
     CU(cudaSetDevice(c->device));
+    e->sm_total = dg::sm_count(c->device);
+    if (const char* rs = std::getenv("DG_RESERVE_SMS")) e->reserve_sms = std::max(0, std::atoi(rs));
+    e->diag_skip_kernel = std::getenv("DG_DIAG_SKIP_KERNEL") != nullptr;
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU(cudaStreamCreateWithFlags(&e->comp, cudaStreamNonBlocking));

@@ -1,0 +1,69 @@
+"""torchrun body for tests/test_multigpu.py: one process per GPU, nodes
+block-partitioned over ranks, NCCL send/recv gossip exchange through libdg.
+Every rank checks its resident nodes bit-exactly against the oracle's fp32
+mirror run of ALL nodes on the CPU (so results are placement-invariant:
+identical to the 1-GPU run).  Small chunks force the chunked, double-buffered
+exchange pipeline.  Exit code 0 = all equal on this rank."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2410_11998_b200 as dg  # noqa: E402
+from oracle import pyoracle as O  # noqa: E402
+
+SEED = 2410
+CFG = {0: dict(alpha=2e-3, beta1=0.974, beta2=0.999, eps=1e-8, s=1),
+       1: dict(alpha=8e-4, beta1=0.9, beta2=0.999, eps=1e-8, s=4)}
+CASES = [("make_one_peer_exponential", "ONE_PEER_EXP", (8,)), ("make_one_peer_ring", "ONE_PEER_RING", (8,)),
+         ("make_static_exponential", "STATIC_EXP", (8,)), ("make_aer", "AER", (8, 2)),
+         ("make_complete", "COMPLETE", (8,)), ("make_one_peer_exponential", "ONE_PEER_EXP", (16,))]
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    d = int(os.environ.get("MP_D", "100003"))
+    chunk = int(os.environ.get("MP_CHUNK", "16384"))
+    T = 12
+    bad = 0
+    for fn, kind, args in CASES:
+        for algo in (0, 1):
+            obj = [dg.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            sched = getattr(dg, fn)(*args)
+            eng = dg.Engine(sched, d, dg.OptimizerConfig(**CFG[algo]), algo=algo, total_steps=T, world_size=world,
+                            rank=rank, device=local, nccl_id=obj[0], chunk=chunk)
+            eng.fill_synthetic(dg.X, SEED, dg.Stream.CONSENSUS_INIT, True, 0)
+            for t in range(1, T + 1):
+                eng.fill_synthetic(dg.G, SEED, dg.Stream.MINIBATCH, True, t)
+                eng.step(t)
+            eng.sync()
+            st = O.init_state(sched.workers(), d, SEED, True, np.float32, algo)
+            O.run(O.make(getattr(O, kind), *args), algo, O.OptimizerConfig(**CFG[algo]), SEED, st, 1, T, T)
+            keys = [("x", dg.X), ("m", dg.M), ("v", dg.V)] + ([("b", dg.ACC)] if algo else [])
+            f = eng.first_node
+            stats = eng.stats()
+            for k, w in keys:
+                got = np.stack([eng.download(i, w) for i in range(eng.local_nodes)])
+                want = st[k][f:f + eng.local_nodes]
+                if not np.array_equal(got.view(np.uint32), want.view(np.uint32)):
+                    print(f"rank {rank}: MISMATCH {fn}{args} algo={algo} {k}", flush=True)
+                    bad += 1
+            print(f"rank {rank}: {fn}{args} algo={algo} nodes {f}..{f + eng.local_nodes - 1} "
+                  f"sent {stats['bytes_sent'] / 1e6:.1f} MB launches {stats['kernel_launches']}", flush=True)
+            eng.close()
+            dist.barrier()
+    dist.destroy_process_group()
+    print(f"rank {rank}: {'ok' if not bad else f'{bad} mismatches'}", flush=True)
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()

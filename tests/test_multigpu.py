@@ -1,0 +1,36 @@
+"""Multi-GPU gossip exchange (NCCL send/recv over NVLink, chunked and
+double-buffered): torchrun one rank per visible GPU (2 or 4), bit-exact vs the
+single-process oracle fp32 mirror for every topology and both algorithms."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+    pytest.skip("needs >= 2 CUDA devices", allow_module_level=True)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", sorted({2, min(4, torch.cuda.device_count())}))
+@pytest.mark.parametrize("d,chunk", [(100_003, 16384), (1 << 20, 0)])
+def test_multigpu_bit_exact(world, d, chunk):
+    if world > torch.cuda.device_count():
+        pytest.skip("not enough GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_parity_main.py")]
+    env = {**os.environ, "MP_D": str(d), "MP_CHUNK": str(chunk)}
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
