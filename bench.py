@@ -47,6 +47,7 @@ def parse():
                    choices=["one_peer_exponential", "one_peer_ring", "static_exponential", "aer"])
     p.add_argument("--algo", choices=["dadam", "accum"], default="dadam")
     p.add_argument("--chunk", type=int, default=0)
+    p.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
     p.add_argument("--e2e-steps", type=int, default=4)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -82,7 +83,10 @@ def config_block(a, world, nodes):
                      f"{a.d:,}-param fp32 bucket per node, {a.algo}"),
         "nodes": nodes, "nodes_per_gpu": a.nodes_per_gpu, "params_per_node": a.d,
         "topology": a.topology, "algo": a.algo, "seed": SEED,
-        "parallelism": f"gossip over {world} GPU(s), nodes block-partitioned, NCCL send/recv over NVLink",
+        "parallelism": (f"gossip over {world} GPU(s), nodes block-partitioned; remote buckets "
+                        + ("read in-kernel from peer HBM over NVLink (CUDA IPC)" if a.transport == "p2p"
+                           else "via chunked NCCL send/recv over NVLink")),
+        "transport": a.transport,
         "l2": "no flush needed: every step streams >= 28 GB per GPU, > 126 MB L2",
         "inputs": "synthetic StreamRng buckets (x0 ConsensusInit, g Minibatch@t=1 held fixed across timed steps)",
     }
@@ -147,9 +151,13 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def step_roofline(sched, world, d, steps_t, hbm_bw, per_update=HBM_PER_UPDATE):
+def step_roofline(sched, world, d, steps_t, hbm_bw, transport, per_update=HBM_PER_UPDATE):
     """SURVEY.md 8(d) per-GPU step bound, summed over the timed rounds:
-    max over GPUs of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL)."""
+    max over GPUs of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL).
+    NCCL transport: every received remote bucket costs 12 B/param of HBM (owner
+    read for the send, recv-slot write, kernel read).  P2P transport: the fused
+    kernel reads remote buckets over NVLink, so HBM pays only the owner-side
+    read (4 B/param per bucket served to a peer)."""
     import paper_2410_11998_b200 as dg
     n = sched.workers()
     total = 0.0
@@ -161,7 +169,11 @@ def step_roofline(sched, world, d, steps_t, hbm_bw, per_update=HBM_PER_UPDATE):
             for g in range(world):
                 sends, recvs = dg.plan_exchange(sched, world, g, r)
                 nl = sum(1 for i in range(n) if i * world // n == g)
-                t_hbm = d * (per_update * nl + HBM_PER_REMOTE * len(recvs)) / hbm_bw
+                if transport == "p2p":
+                    remote_hbm = 4.0 * len(sends)
+                else:
+                    remote_hbm = HBM_PER_REMOTE * len(recvs)
+                t_hbm = d * (per_update * nl + remote_hbm) / hbm_bw
                 t_nvl = 4.0 * d * max(len(recvs), len(sends)) / NVL_MEASURED
                 worst = max(worst, t_hbm, t_nvl)
             cache[r] = worst
@@ -270,7 +282,8 @@ def run_ours(a):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     eng = dg.Engine(sched, a.d, dg.OptimizerConfig(**h), algo=algo, total_steps=total_t, world_size=world,
-                    rank=rank, device=local, nccl_id=nccl_id, chunk=a.chunk)
+                    rank=rank, device=local, nccl_id=nccl_id, chunk=a.chunk,
+                    transport=dg.TRANSPORT_P2P if a.transport == "p2p" else dg.TRANSPORT_NCCL)
     eng.fill_synthetic(dg.X, SEED, dg.Stream.CONSENSUS_INIT, True, 0)
     eng.fill_synthetic(dg.G, SEED, dg.Stream.MINIBATCH, True, 1)
     eng.sync()
@@ -328,7 +341,8 @@ def run_ours(a):
     kern_s = st["kernel_ms"] / 1e3
     achieved = st["timed_hbm_bytes"] / kern_s if kern_s > 0 else 0.0
     per_launch = st["timed_hbm_bytes"] / max(1, st["timed_launches"])
-    roof_step_s = step_roofline(sched, world, a.d, timed_t, hbm_bw)
+    transport = "p2p" if st["transport"] == dg.TRANSPORT_P2P else "nccl"
+    roof_step_s = step_roofline(sched, world, a.d, timed_t, hbm_bw, transport)
 
     # ---- end to end through the public API: pinned host g -> H2D each step, step, D2H status
     e2e = None
@@ -375,7 +389,9 @@ def run_ours(a):
                          "peak_source": peak_src, "kernel": "gossip_adam_fused"},
             "step_roofline": {"bound_ms_per_step": 1e3 * roof_step_s / a.steps,
                               "frac": (roof_step_s * 1e3) / ms_max,
-                              "model": "SURVEY.md 8(d): max over GPUs of max(HBM bytes/BW_HBM, NVLink bytes/770 GB/s)"},
+                              "model": ("SURVEY.md 8(d): per round, max over GPUs of max(HBM bytes/BW_HBM, "
+                                        f"NVLink bytes/770 GB/s), {transport} transport"),
+                              "nvlink_bytes_received_per_step": st["bytes_received"] / max(1, st["steps"])},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
             "nvlink_bytes_sent_per_step": st["bytes_sent"] / max(1, st["steps"]),
             "nccl_version": st["nccl_version"],

@@ -151,7 +151,16 @@ typedef struct dg_engine_config {
   int algo;                    /* DG_ALGO_DADAM | DG_ALGO_ACCUM */
   dg_adam_cfg adam;
   long total_steps;            /* T (AccumAdam requires T mod s == 0) */
+  int transport;               /* DG_TRANSPORT_*: how remote neighbour buckets move (world_size > 1) */
 } dg_engine_config;
+
+/* DG_TRANSPORT_P2P (default): the fused kernel reads remote neighbours'
+ * x^(t-1) directly from peer HBM over NVLink (CUDA IPC mappings; x is
+ * double-buffered in exchange rounds, a stream-ordered 1-element NCCL
+ * all-reduce is the cross-GPU step barrier).  DG_TRANSPORT_NCCL: chunked
+ * ncclSend/ncclRecv into double-buffered recv slots on a side stream,
+ * overlapped with the fused kernel on the previous chunk. */
+enum { DG_TRANSPORT_AUTO = 0, DG_TRANSPORT_NCCL = 1, DG_TRANSPORT_P2P = 2 };
 
 typedef struct dg_engine_stats {
   int local_nodes, first_node, nodes, world_size, rank;
@@ -165,6 +174,8 @@ typedef struct dg_engine_stats {
   double kernel_ms;         /* summed CUDA-event durations of timed fused launches */
   long timed_launches;      /* launches covered by kernel_ms / timed_hbm_bytes */
   double timed_hbm_bytes;   /* algorithmic HBM bytes of those launches */
+  int transport;            /* DG_TRANSPORT_NCCL | DG_TRANSPORT_P2P (1-GPU engines report P2P) */
+  long barriers;            /* cross-GPU step barriers issued */
 } dg_engine_stats;
 
 /* ncclGetUniqueId (call on rank 0, broadcast the 128 bytes to all ranks) */

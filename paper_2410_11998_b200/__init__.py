@@ -27,6 +27,7 @@ __all__ = [
     "validate", "spectral_lambda", "effective_lambda", "OptimizerConfig", "gossip_mix",
     "dadam_step", "accum_adam_step", "check_divergence", "fill_synthetic", "Engine",
     "nccl_unique_id", "plan_exchange", "library_path", "DADAM", "ACCUM",
+    "TRANSPORT_AUTO", "TRANSPORT_NCCL", "TRANSPORT_P2P",
     "X", "G", "M", "V", "ACC", "Stream",
 ]
 
@@ -35,6 +36,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg.so")
 
 DADAM, ACCUM = 0, 1
+TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_P2P = 0, 1, 2
 X, G, M, V, ACC = 0, 1, 2, 3, 4
 
 
@@ -92,7 +94,7 @@ class _EngineConfig(C.Structure):
     _fields_ = [("schedule", C.c_void_p), ("world_size", C.c_int), ("rank", C.c_int),
                 ("device", C.c_int), ("nccl_id", C.c_void_p), ("d", C.c_size_t),
                 ("chunk", C.c_size_t), ("algo", C.c_int), ("adam", _AdamCfg),
-                ("total_steps", C.c_long)]
+                ("total_steps", C.c_long), ("transport", C.c_int)]
 
 
 class _EngineStats(C.Structure):
@@ -101,7 +103,8 @@ class _EngineStats(C.Structure):
                 ("chunk", C.c_size_t), ("kernel_launches", C.c_long), ("steps", C.c_long),
                 ("bytes_sent", C.c_double), ("bytes_received", C.c_double),
                 ("hbm_bytes", C.c_double), ("nccl_version", C.c_long), ("kernel_ms", C.c_double),
-                ("timed_launches", C.c_long), ("timed_hbm_bytes", C.c_double)]
+                ("timed_launches", C.c_long), ("timed_hbm_bytes", C.c_double), ("transport", C.c_int),
+                ("barriers", C.c_long)]
 
 
 _lib = None
@@ -411,14 +414,14 @@ class Engine:
 
     def __init__(self, schedule: MixingSchedule, d: int, cfg: OptimizerConfig, algo: int = DADAM,
                  total_steps: int = 0, world_size: int = 1, rank: int = 0, device: int = 0,
-                 nccl_id: Optional[bytes] = None, chunk: int = 0):
+                 nccl_id: Optional[bytes] = None, chunk: int = 0, transport: int = TRANSPORT_AUTO):
         self.schedule = schedule
         idbuf = None
         if nccl_id is not None:
             idbuf = (C.c_char * 128).from_buffer_copy(nccl_id)
         ec = _EngineConfig(schedule.handle.value, world_size, rank, device,
                            C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
-                           d, chunk, algo, cfg._c(), total_steps)
+                           d, chunk, algo, cfg._c(), total_steps, transport)
         h = C.c_void_p()
         _check(lib().dg_engine_create(C.byref(ec), C.byref(h)))
         self._h = h

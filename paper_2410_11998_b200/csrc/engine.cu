@@ -423,7 +423,17 @@ struct dg_engine {
   void harvest_timing();
 
   float* x_alt = nullptr;  // second x buffer (ping-pong rounds)
-  int xcur = 0;            // which x buffer holds the current x
+  int xcur = 0;            // which x buffer holds the current x (identical on every rank)
+  // P2P transport: every rank's two x buffers mapped into this process (CUDA IPC)
+  int transport = DG_TRANSPORT_P2P;
+  std::vector<float*> peer_base[2];  // [buffer][rank]; own rank = own pointers
+  std::vector<char> round_remote;    // per round: any rank mixes a remote bucket
+  float* bar_buf = nullptr;          // 1-element all-reduce = cross-GPU step barrier
+  long barriers = 0;
+  const float* peer_x(int node) const {
+    const int owner = dg::owner_of(node, N, G);
+    return peer_base[xcur][owner] + size_t(node - dg::first_node_of(owner, N, G)) * d_pad;
+  }
   float* buf(int which, int local) const {
     const float* base = (which == DG_BUF_X && xcur) ? x_alt : arena[which];
     return const_cast<float*>(base) + size_t(local) * d_pad;
@@ -452,6 +462,10 @@ dg_engine::~dg_engine() {
     if (a) cudaFree(a);
   if (slots) cudaFree(slots);
   if (x_alt) cudaFree(x_alt);
+  if (bar_buf) cudaFree(bar_buf);
+  for (int b = 0; b < 2; ++b)
+    for (int r = 0; r < int(peer_base[b].size()); ++r)
+      if (r != rank && peer_base[b][r]) cudaIpcCloseMemHandle(peer_base[b][r]);
   if (flag) cudaFree(flag);
   if (ev_begin) cudaEventDestroy(ev_begin);
   for (auto e : ev_slot_free)
@@ -479,7 +493,8 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   }
   const float* slot_ptr[dg::kMaxRemote];
   for (int r = 0; r < int(p.recv_node.size()); ++r)
-    slot_ptr[r] = slots + (size_t(slot_set) * max_recv + r) * chunk;
+    slot_ptr[r] = transport == DG_TRANSPORT_P2P ? peer_x(p.recv_node[r]) + off
+                                                : slots + (size_t(slot_set) * max_recv + r) * chunk;
   const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr};
   const bool tma = dg::use_tma(p);
   LaunchFnHolder fnh{nullptr};
@@ -487,8 +502,11 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
     dg::fill_args(argbuf, p, bf, off, len, s, int(t), flag);
     fnh.fn = dg::pick(p.comp_size, p.src_bound, algo, fold);
   }
+  // algorithmic LOCAL HBM bytes of this launch (remote buckets: recv-slot reads
+  // for NCCL; for P2P they come over NVLink and are counted in `received`)
   const double per = algo == DG_ALGO_DADAM ? 28.0 : (fold ? 36.0 : 28.0);
-  const double bytes = double(len) * (per * p.n_local + 4.0 * double(p.recv_node.size()));
+  const double remote_hbm = transport == DG_TRANSPORT_P2P ? 0.0 : 4.0 * double(p.recv_node.size());
+  const double bytes = double(len) * (per * p.n_local + remote_hbm);
   if (timing) {
     if (tev_used == tev.size()) {
       cudaEvent_t a, b;
@@ -527,8 +545,25 @@ void dg_engine::step(long t) {
   bool fold = false;
   const dg::DevScalars s = dg::scalars(&adam, algo, t, T, &fold);
   CU(cudaSetDevice(device));
-  const dg::RoundPlan& p = plans[size_t((t - 1) % P)];
+  const size_t ri = size_t((t - 1) % P);
+  const dg::RoundPlan& p = plans[ri];
   ++steps;
+  if (transport == DG_TRANSPORT_P2P && G > 1) {
+    // Cross-GPU step barrier, stream-ordered on the compute stream, before any
+    // step that reads peers' x^(t-1) (their step t-1 must be complete) and
+    // before the step after one (peers must have finished reading the buffer
+    // this step may overwrite).  Every rank takes the same decision.
+    const size_t prev = size_t((t - 2 + P) % P);
+    if (round_remote[ri] || (t > 1 && round_remote[prev])) {
+      NC(ncclAllReduce(bar_buf, bar_buf, 1, ncclFloat, ncclSum, nccl, comp));
+      ++barriers;
+    }
+    enqueue_fused(p, 0, d, 0, s, fold, t);  // remote sources read over NVLink inside the kernel
+    sent += 4.0 * double(d) * double(p.send_node.size());
+    received += 4.0 * double(d) * double(p.recv_node.size());
+    if (p.pingpong) xcur ^= 1;
+    return;
+  }
   if (p.send_node.empty() && p.recv_node.empty()) {  // intra-GPU round: one launch
     enqueue_fused(p, 0, d, 0, s, fold, t);
     if (p.pingpong) xcur ^= 1;
@@ -609,17 +644,31 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       e->max_recv = std::max(e->max_recv, int(e->plans.back().recv_node.size()));
     }
     e->NL = e->plans[0].n_local;
-    // rounds with mixing components of >= DG_PINGPONG_MIN_NC members (default 4)
-    // run with x double-buffered (one lean gather per node instead of one
-    // thread carrying a whole component)
+    e->transport = c->transport == DG_TRANSPORT_NCCL ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
+    if (const char* tr = std::getenv("DG_TRANSPORT"))
+      e->transport = std::string(tr) == "nccl" ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
+    const bool p2p = e->transport == DG_TRANSPORT_P2P && e->G > 1;
+    // x double-buffered ("ping-pong") rounds: mixing components of >=
+    // DG_PINGPONG_MIN_NC members (default 4) anywhere, and with the P2P transport
+    // every round in which any rank reads a remote bucket.  Decided from the
+    // global schedule so that every rank flips its x buffer identically.
     const char* ppenv = std::getenv("DG_PINGPONG_MIN_NC");
     const int pp_min = ppenv ? std::atoi(ppenv) : 4;
     bool any_pp = false;
-    for (auto& p : e->plans)
-      if (pp_min > 0 && p.comp_size >= pp_min) {
-        dg::make_pingpong(p, e->first);
+    e->round_remote.assign(e->P, 0);
+    for (int r = 0; r < e->P; ++r) {
+      bool pp = false;
+      for (int g = 0; g < e->G; ++g) {
+        const auto q = g == e->rank ? e->plans[r] : dg::build_round_plan(*c->schedule, e->G, g, r + 1);
+        if (pp_min > 0 && q.comp_size >= pp_min) pp = true;
+        if (!q.recv_node.empty()) e->round_remote[r] = 1;
+      }
+      if (p2p && e->round_remote[r]) pp = true;
+      if (pp) {
+        dg::make_pingpong(e->plans[r], e->first);
         any_pp = true;
       }
+    }
     if (e->NL < 1) dg::config_error("engine_create: no resident nodes on this rank");
     CU(cudaSetDevice(c->device));
     e->sm_total = dg::sm_count(c->device);
@@ -638,11 +687,11 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       CU(cudaMalloc(&e->arena[k], sizeof(float) * e->d_pad * e->NL));
       CU(cudaMemsetAsync(e->arena[k], 0, sizeof(float) * e->d_pad * e->NL, e->comp));
     }
-    if (any_pp) {
+    if (any_pp || p2p) {
       CU(cudaMalloc(&e->x_alt, sizeof(float) * e->d_pad * e->NL));
       CU(cudaMemsetAsync(e->x_alt, 0, sizeof(float) * e->d_pad * e->NL, e->comp));
     }
-    if (e->max_recv) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
+    if (e->max_recv && !p2p) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
     CU(cudaMalloc(&e->flag, sizeof(int)));
     const int none = INT_MAX;
     CU(cudaMemcpyAsync(e->flag, &none, sizeof(int), cudaMemcpyHostToDevice, e->comp));
@@ -651,6 +700,35 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       ncclUniqueId id;
       std::memcpy(&id, c->nccl_id, sizeof(id));
       NC(ncclCommInitRank(&e->nccl, e->G, id, e->rank));
+    }
+    for (int b = 0; b < 2; ++b) e->peer_base[b].assign(e->G, nullptr);
+    e->peer_base[0][e->rank] = e->arena[DG_BUF_X];
+    e->peer_base[1][e->rank] = e->x_alt;
+    if (p2p) {
+      // exchange CUDA IPC handles of both x buffers (one 128-byte record per rank)
+      static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+      std::vector<char> mine(128), all(128 * size_t(e->G));
+      CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data()), e->arena[DG_BUF_X]));
+      CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + 64), e->x_alt));
+      char* dbuf = nullptr;
+      CU(cudaMalloc(&dbuf, all.size()));
+      CU(cudaMemcpy(dbuf + 128 * size_t(e->rank), mine.data(), 128, cudaMemcpyHostToDevice));
+      NC(ncclAllGather(dbuf + 128 * size_t(e->rank), dbuf, 128, ncclChar, e->nccl, e->comp));
+      CU(cudaStreamSynchronize(e->comp));
+      CU(cudaMemcpy(all.data(), dbuf, all.size(), cudaMemcpyDeviceToHost));
+      CU(cudaFree(dbuf));
+      for (int g = 0; g < e->G; ++g) {
+        if (g == e->rank) continue;
+        for (int b = 0; b < 2; ++b) {
+          cudaIpcMemHandle_t h;
+          std::memcpy(&h, all.data() + 128 * size_t(g) + 64 * b, 64);
+          void* ptr = nullptr;
+          CU(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+          e->peer_base[b][g] = static_cast<float*>(ptr);
+        }
+      }
+      CU(cudaMalloc(&e->bar_buf, sizeof(float)));
+      CU(cudaMemset(e->bar_buf, 0, sizeof(float)));
     }
     *out = e.release();
   });
@@ -761,6 +839,8 @@ int dg_engine_get_stats(const dg_engine* e, dg_engine_stats* o) {
     o->kernel_ms = e->kernel_ms;
     o->timed_launches = e->timed_launches;
     o->timed_hbm_bytes = e->timed_bytes;
+    o->transport = e->transport;
+    o->barriers = e->barriers;
   });
 }
 

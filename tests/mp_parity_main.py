@@ -17,6 +17,7 @@ import paper_2410_11998_b200 as dg  # noqa: E402
 from oracle import pyoracle as O  # noqa: E402
 
 SEED = 2410
+TRANSPORT = {"nccl": dg.TRANSPORT_NCCL, "p2p": dg.TRANSPORT_P2P}[os.environ.get("MP_TRANSPORT", "p2p")]
 CFG = {0: dict(alpha=2e-3, beta1=0.974, beta2=0.999, eps=1e-8, s=1),
        1: dict(alpha=8e-4, beta1=0.9, beta2=0.999, eps=1e-8, s=4)}
 CASES = [("make_one_peer_exponential", "ONE_PEER_EXP", (8,)), ("make_one_peer_ring", "ONE_PEER_RING", (8,)),
@@ -39,7 +40,7 @@ def main():
             dist.broadcast_object_list(obj, src=0)
             sched = getattr(dg, fn)(*args)
             eng = dg.Engine(sched, d, dg.OptimizerConfig(**CFG[algo]), algo=algo, total_steps=T, world_size=world,
-                            rank=rank, device=local, nccl_id=obj[0], chunk=chunk)
+                            rank=rank, device=local, nccl_id=obj[0], chunk=chunk, transport=TRANSPORT)
             eng.fill_synthetic(dg.X, SEED, dg.Stream.CONSENSUS_INIT, True, 0)
             for t in range(1, T + 1):
                 eng.fill_synthetic(dg.G, SEED, dg.Stream.MINIBATCH, True, t)
@@ -56,8 +57,9 @@ def main():
                 if not np.array_equal(got.view(np.uint32), want.view(np.uint32)):
                     print(f"rank {rank}: MISMATCH {fn}{args} algo={algo} {k}", flush=True)
                     bad += 1
-            print(f"rank {rank}: {fn}{args} algo={algo} nodes {f}..{f + eng.local_nodes - 1} "
-                  f"sent {stats['bytes_sent'] / 1e6:.1f} MB launches {stats['kernel_launches']}", flush=True)
+            print(f"rank {rank}: {fn}{args} algo={algo} transport={stats['transport']} nodes {f}..{f + eng.local_nodes - 1} "
+                  f"sent {stats['bytes_sent'] / 1e6:.1f} MB launches {stats['kernel_launches']} "
+                  f"barriers {stats['barriers']}", flush=True)
             eng.close()
             dist.barrier()
     dist.destroy_process_group()
