@@ -192,6 +192,11 @@ int dg_engine_upload(dg_engine* e, int local_node, int which, const float* host,
                      size_t count);
 int dg_engine_download(dg_engine* e, int local_node, int which, float* host, size_t offset,
                        size_t count);
+/* out[k] = buffer `which` of resident node `local_node` at element idx[k]
+ * (host index array, n entries; synchronous).  Sampled checkpoints / parity
+ * checks of full-size buckets without copying them whole. */
+int dg_engine_gather(dg_engine* e, int local_node, int which, const uint64_t* idx, size_t n,
+                     float* out);
 /* Fill buffer `which` of every resident node with synthetic values of
  * StreamRng(seed, purpose, worker, iteration): worker = global node id when
  * per_node != 0, else 0 (shared x^(0), Alg. 1 line 1). */

@@ -428,6 +428,50 @@ int run(const or_sched* s, int algo, const or_adam_cfg* cfg, uint64_t seed, size
   return OR_OK;
 }
 
+// Column-sampled run (see oracle.h): same per-element arithmetic as step_all.
+template <class T>
+int run_cols(const or_sched* s, int algo, const or_adam_cfg* cfg, uint64_t seed,
+             const uint64_t* cols, size_t nc, int dispersed, long t0, long t1, long T_, int threads,
+             T* x, T* m, T* v, T* b) {
+  if (!s) return fail(OR_CONFIG_ERROR, "run_cols: empty schedule");
+  if (algo == OR_ACCUM && !b) return fail(OR_CONFIG_ERROR, "run_cols: accumulator buffer missing");
+  set_threads(threads);
+  const int n = s->workers;
+  for (int i = 0; i < n; ++i) {  // x^(0)
+    const uint64_t st = dispersed ? stream_state(seed, 6u, uint64_t(i), 0) : stream_state(seed, 4u, 0, 0);
+    for (size_t c = 0; c < nc; ++c) x[size_t(i) * nc + c] = T(bucket_value(draw(st, cols[c])));
+  }
+  std::vector<T> xprev(size_t(n) * nc);
+  for (long t = t0; t <= t1; ++t) {
+    Scalars sc;
+    if (int rc = scalars(cfg, algo, t, T_, &sc, sizeof(T) == 4)) return rc;
+    const TS<T> ts(sc);
+    const Mat& w = *round_mat(s, t);
+    const auto& nb = *round_nbrs(s, t);
+    std::memcpy(xprev.data(), x, sizeof(T) * xprev.size());
+    const bool fold = algo == OR_ACCUM && (t % cfg->s == 0);
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (int i = 0; i < n; ++i) {
+      std::vector<T> mixed(nc), g(nc);
+      const uint64_t st = stream_state(seed, 2u, uint64_t(i), uint64_t(t));
+      for (size_t c = 0; c < nc; ++c) g[c] = T(bucket_value(draw(st, cols[c])));
+      mix_into(mixed.data(), xprev.data(), nc, nb[i], w, i);
+      const size_t o = size_t(i) * nc;
+      if (algo == OR_DADAM)
+        dadam_elems(x + o, g.data(), m + o, v + o, mixed.data(), nc, ts);
+      else
+        accum_elems(x + o, g.data(), m + o, v + o, b + o, mixed.data(), nc, ts, fold);
+      if (!all_finite(x + o, nc) || !all_finite(m + o, nc) || !all_finite(v + o, nc)) bad = 1;
+    }
+    if (bad) {
+      g_div_iter = t;
+      return fail(OR_DIVERGENCE, "non-finite state at iteration " + std::to_string(t));
+    }
+  }
+  return OR_OK;
+}
+
 }  // namespace
 
 // ================================================================= extern "C"
@@ -713,6 +757,16 @@ int or_step_all_f64(const or_sched* s, int algo, const or_adam_cfg* cfg, size_t 
   if (!s) return fail(OR_CONFIG_ERROR, "step_all: empty schedule");
   set_threads(threads);
   return step_all<double>(s, algo, cfg, d, t, T, 0, false, g, x, xprev, m, v, b);
+}
+int or_run_cols_f32(const or_sched* s, int algo, const or_adam_cfg* cfg, uint64_t seed,
+                    const uint64_t* cols, size_t nc, int dispersed, long t0, long t1, long T,
+                    int threads, float* x, float* m, float* v, float* b) {
+  return run_cols<float>(s, algo, cfg, seed, cols, nc, dispersed, t0, t1, T, threads, x, m, v, b);
+}
+int or_run_cols_f64(const or_sched* s, int algo, const or_adam_cfg* cfg, uint64_t seed,
+                    const uint64_t* cols, size_t nc, int dispersed, long t0, long t1, long T,
+                    int threads, double* x, double* m, double* v, double* b) {
+  return run_cols<double>(s, algo, cfg, seed, cols, nc, dispersed, t0, t1, T, threads, x, m, v, b);
 }
 int or_max_threads(void) {
 #ifdef _OPENMP

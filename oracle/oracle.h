@@ -107,6 +107,20 @@ int or_step_all_f64(const or_sched* s, int algo, const or_adam_cfg* cfg, size_t 
                     double* v, double* b);
 int or_max_threads(void);
 
+/* Column-sampled run: every parameter column evolves independently of the
+ * others (mixing and Adam are elementwise), so the trajectory of the columns
+ * cols[0..ncols) of a d-parameter bucket can be replayed exactly without the
+ * rest of the bucket.  x0 and g_i^(t) are drawn at the columns' own draw
+ * indices (x0: ConsensusInit per node if dispersed, else the shared InitModel
+ * stream).  Outputs are n x ncols row-major, fp32 mirror (_f32) or fp64 with
+ * the same fp32 inputs (_f64).  Used to check full-size (125M .. 1.3B) buckets. */
+int or_run_cols_f32(const or_sched* s, int algo, const or_adam_cfg* cfg, uint64_t seed,
+                    const uint64_t* cols, size_t ncols, int dispersed, long t_begin, long t_end,
+                    long T, int threads, float* x, float* m, float* v, float* b);
+int or_run_cols_f64(const or_sched* s, int algo, const or_adam_cfg* cfg, uint64_t seed,
+                    const uint64_t* cols, size_t ncols, int dispersed, long t_begin, long t_end,
+                    long T, int threads, double* x, double* m, double* v, double* b);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,10 @@ def lib():
             getattr(L, f"or_run_{nm}").argtypes = [C.c_void_p, C.c_int, C.POINTER(AdamCfg), C.c_uint64,
                                                    C.c_size_t, C.c_long, C.c_long, C.c_long, C.c_int,
                                                    p, p, p, C.c_void_p]
+        for nm, p in (("f64", _dp), ("f32", _fp)):
+            getattr(L, f"or_run_cols_{nm}").argtypes = [C.c_void_p, C.c_int, C.POINTER(AdamCfg), C.c_uint64, _u64p,
+                                                        C.c_size_t, C.c_int, C.c_long, C.c_long, C.c_long,
+                                                        C.c_int, p, p, p, C.c_void_p]
         L.or_step_all_f64.argtypes = [C.c_void_p, C.c_int, C.POINTER(AdamCfg), C.c_size_t, C.c_long,
                                       C.c_long, C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_void_p]
         _lib = L
@@ -329,3 +333,17 @@ def ref_run(s, algo, cfg, seed, state, t_begin, t_end, T=0, threads=0, g_fixed=N
     if rc != OK:
         raise OracleError(rc, R.ref_last_error().decode())
     return el.value
+
+
+def run_cols(s, algo, cfg, seed, cols, dispersed, t_begin, t_end, T=0, dtype=np.float32, threads=0):
+    """Replay the columns `cols` of a full-size bucket (oracle.h or_run_cols_*).
+    Returns {"x","m","v"[,"b"]} arrays of shape (workers, len(cols))."""
+    cols = np.ascontiguousarray(cols, np.uint64)
+    n, nc = s.workers, cols.size
+    st = {k: np.zeros((n, nc), dtype) for k in ("x", "m", "v")}
+    st["b"] = np.zeros((n, nc), dtype) if algo == ACCUM else None
+    fn = lib().or_run_cols_f32 if dtype == np.float32 else lib().or_run_cols_f64
+    c = cfg.c()
+    _check(fn(s.handle, algo, C.byref(c), seed, cols, nc, int(dispersed), t_begin, t_end, T, threads,
+              st["x"].reshape(-1), st["m"].reshape(-1), st["v"].reshape(-1), _ptr(st["b"])))
+    return st

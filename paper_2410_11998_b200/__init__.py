@@ -141,6 +141,7 @@ SIGNATURES = {
     "dg_engine_upload": ([_VP, _I, _I, _VP, _SZ, _SZ], _I),
     "dg_engine_download": ([_VP, _I, _I, _VP, _SZ, _SZ], _I),
     "dg_engine_fill_synthetic": ([_VP, _I, C.c_uint64, C.c_uint32, _I, C.c_uint64], _I),
+    "dg_engine_gather": ([_VP, _I, _I, _VP, _SZ, _VP], _I),
     "dg_engine_step": ([_VP, _L], _I),
     "dg_engine_sync": ([_VP], _I),
     "dg_engine_streams": ([_VP, C.POINTER(_VP), C.POINTER(_VP)], _I),
@@ -453,6 +454,13 @@ class Engine:
         count = self.d - offset if count is None else count
         out = np.empty(count, np.float32)
         _check(lib().dg_engine_download(self._h, local, which, out.ctypes.data_as(_VP), offset, count))
+        return out
+
+    def gather(self, local: int, which: int, idx) -> np.ndarray:
+        idx = np.ascontiguousarray(idx, np.uint64)
+        out = np.empty(idx.size, np.float32)
+        _check(lib().dg_engine_gather(self._h, local, which, idx.ctypes.data_as(_VP), idx.size,
+                                      out.ctypes.data_as(_VP)))
         return out
 
     def fill_synthetic(self, which: int, seed: int, purpose: int, per_node: bool, iteration: int):

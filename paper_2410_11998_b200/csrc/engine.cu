@@ -645,9 +645,12 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     }
     e->NL = e->plans[0].n_local;
     e->transport = c->transport == DG_TRANSPORT_NCCL ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
-    if (const char* tr = std::getenv("DG_TRANSPORT"))
+    bool auto_transport = c->transport == DG_TRANSPORT_AUTO;
+    if (const char* tr = std::getenv("DG_TRANSPORT")) {
       e->transport = std::string(tr) == "nccl" ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
-    const bool p2p = e->transport == DG_TRANSPORT_P2P && e->G > 1;
+      auto_transport = false;
+    }
+    bool p2p = e->transport == DG_TRANSPORT_P2P && e->G > 1;
     // x double-buffered ("ping-pong") rounds: mixing components of >=
     // DG_PINGPONG_MIN_NC members (default 4) anywhere, and with the P2P transport
     // every round in which any rank reads a remote bucket.  Decided from the
@@ -704,7 +707,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     for (int b = 0; b < 2; ++b) e->peer_base[b].assign(e->G, nullptr);
     e->peer_base[0][e->rank] = e->arena[DG_BUF_X];
     e->peer_base[1][e->rank] = e->x_alt;
-    if (p2p) {
+    if (p2p) try {
       // exchange CUDA IPC handles of both x buffers (one 128-byte record per rank)
       static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
       std::vector<char> mine(128), all(128 * size_t(e->G));
@@ -729,6 +732,20 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       }
       CU(cudaMalloc(&e->bar_buf, sizeof(float)));
       CU(cudaMemset(e->bar_buf, 0, sizeof(float)));
+    } catch (const dg::Error& err) {
+      // AUTO: no CUDA IPC between these processes -> chunked NCCL send/recv.
+      // (IPC success/failure is a property of the node, identical on all ranks.)
+      if (!auto_transport) throw;
+      cudaGetLastError();
+      for (int g = 0; g < e->G; ++g)
+        for (int b = 0; b < 2; ++b)
+          if (g != e->rank && e->peer_base[b][g]) {
+            cudaIpcCloseMemHandle(e->peer_base[b][g]);
+            e->peer_base[b][g] = nullptr;
+          }
+      e->transport = DG_TRANSPORT_NCCL;
+      p2p = false;
+      if (e->max_recv) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
     }
     *out = e.release();
   });
@@ -765,6 +782,29 @@ int dg_engine_download(dg_engine* e, int local, int which, float* host, size_t o
     CU(cudaSetDevice(e->device));
     CU(cudaMemcpyAsync(host, e->buf(which, local) + off, cnt * sizeof(float), cudaMemcpyDeviceToHost,
                        e->comp));
+    CU(cudaStreamSynchronize(e->comp));
+  });
+}
+
+int dg_engine_gather(dg_engine* e, int local, int which, const uint64_t* idx, size_t n, float* out) {
+  return guarded([&] {
+    check_slice(e, local, which, 0, 0);
+    if (n && (!idx || !out)) dg::config_error("engine_gather: null argument");
+    for (size_t k = 0; k < n; ++k)
+      if (idx[k] >= e->d) dg::config_error("engine_gather: index out of range");
+    if (!n) return;
+    CU(cudaSetDevice(e->device));
+    uint64_t* didx = nullptr;
+    float* dout = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&didx), n * sizeof(uint64_t), e->comp));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&dout), n * sizeof(float), e->comp));
+    CU(cudaMemcpyAsync(didx, idx, n * sizeof(uint64_t), cudaMemcpyHostToDevice, e->comp));
+    dg::gather_kernel<<<unsigned((n + 255) / 256), 256, 0, e->comp>>>(dout, e->buf(which, local), didx,
+                                                                       (long long)n);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out, dout, n * sizeof(float), cudaMemcpyDeviceToHost, e->comp));
+    CU(cudaFreeAsync(didx, e->comp));
+    CU(cudaFreeAsync(dout, e->comp));
     CU(cudaStreamSynchronize(e->comp));
   });
 }

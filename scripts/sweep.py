@@ -14,8 +14,7 @@ runs = [("default", dict(base))]
 for lib in sorted(glob.glob(os.path.join(ROOT, "build", "variants", "libdg_*.so"))):
     runs.append((os.path.basename(lib)[6:-3], {**base, "DG_LIB": lib}))
 if not base:
-    runs.append(("pp_all", {"DG_PINGPONG_MIN_NC": "1"}))
-    runs.append(("pp_off", {"DG_PINGPONG_MIN_NC": "0"}))
+    runs.append(("waves2", {"DG_WAVES": "2"}))
 for name, env in runs:
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "30", "--warmup", "4", "--no-e2e",
            "--no-cpu-baseline"] + extra

@@ -25,11 +25,39 @@ CASES = [("make_one_peer_exponential", "ONE_PEER_EXP", (8,)), ("make_one_peer_ri
          ("make_complete", "COMPLETE", (8,)), ("make_one_peer_exponential", "ONE_PEER_EXP", (16,))]
 
 
+def fullsize(rank, world, local):
+    """BASELINE configs 4 (AER(8,2), 1.3B, AccumAdam s=4) and 5 (64 nodes one-peer
+    exponential, 125M per node; needs 4 GPUs) at full size, sampled columns."""
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from conftest import normwise
+    from fullsize import check_against_oracle, run_engine_cols, sample_columns
+    cases = [("config4_aer_1.3B_accum", "make_aer", "AER", (8, 2), 1_300_000_000, 1, 8)]
+    if world >= 4:
+        cases.append(("config5_64nodes_125M", "make_one_peer_exponential", "ONE_PEER_EXP", (64,), 125_000_000, 0, 12))
+    bad = 0
+    for name, fn, kind, args, d, algo, T in cases:
+        obj = [dg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        cols = sample_columns(d)
+        got, first, nl = run_engine_cols(dg, getattr(dg, fn)(*args), d, algo, T, cols, world_size=world,
+                                         rank=rank, device=local, nccl_id=obj[0], transport=TRANSPORT)
+        errs = check_against_oracle(O, O.make(getattr(O, kind), *args), algo, T, cols, got, first, nl, normwise)
+        print(f"rank {rank}: {name} nodes {first}..{first + nl - 1}: {'ok' if not errs else errs[:3]}", flush=True)
+        bad += len(errs)
+        dist.barrier()
+    return bad
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
+    if os.environ.get("MP_FULLSIZE"):
+        bad = fullsize(rank, world, local)
+        dist.destroy_process_group()
+        print(f"rank {rank}: {'ok' if not bad else f'{bad} failures'}", flush=True)
+        sys.exit(1 if bad else 0)
     d = int(os.environ.get("MP_D", "100003"))
     chunk = int(os.environ.get("MP_CHUNK", "16384"))
     T = 12

@@ -1,0 +1,27 @@
+"""Parity at BASELINE.json's full bucket sizes (configs 2 and 3 on one GPU):
+the engine runs the whole bucket; a 32k-column sample (incl. both ends) is
+compared bit-exactly with the oracle's fp32 mirror replay of those columns and
+norm-wise (<= 1e-6) with fp64.  Configs 4 and 5 need >= 2 / 4 GPUs
+(tests/test_multigpu.py::test_fullsize_*)."""
+import pytest
+
+from conftest import normwise
+from fullsize import check_against_oracle, run_engine_cols, sample_columns
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+@pytest.mark.parametrize("name,fn,kind,args,d,algo,T", [
+    ("config2_one_peer_exp_125M", "make_one_peer_exponential", "ONE_PEER_EXP", (8,), 125_000_000, 0, 12),
+    ("config3_static_exp_350M", "make_static_exponential", "STATIC_EXP", (8,), 350_000_000, 0, 6),
+    ("config2_accum_125M", "make_one_peer_exponential", "ONE_PEER_EXP", (8,), 125_000_000, 1, 8),
+])
+def test_fullsize_single_gpu(dg, oracle, name, fn, kind, args, d, algo, T):
+    cols = sample_columns(d)
+    got, first, nl = run_engine_cols(dg, getattr(dg, fn)(*args), d, algo, T, cols)
+    bad = check_against_oracle(oracle, oracle.make(getattr(oracle, kind), *args), algo, T, cols, got, first,
+                               nl, normwise)
+    assert not bad, (name, bad[:5])

@@ -35,3 +35,15 @@ def test_multigpu_bit_exact(world, d, chunk, transport):
     env = {**os.environ, "MP_D": str(d), "MP_CHUNK": str(chunk), "MP_TRANSPORT": transport}
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("transport", ["p2p"])
+def test_fullsize_configs_4_and_5(transport):
+    """BASELINE config 4 (AER, 1.3B/node, AccumAdam s=4) on all visible GPUs (2 or 4) and
+    config 5 (64 nodes x 125M, one-peer exponential) when 4 GPUs are visible."""
+    world = min(4, torch.cuda.device_count())
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_parity_main.py")]
+    env = {**os.environ, "MP_FULLSIZE": "1", "MP_TRANSPORT": transport}
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
