@@ -202,6 +202,12 @@ int dg_engine_gather(dg_engine* e, int local_node, int which, const uint64_t* id
  * per_node != 0, else 0 (shared x^(0), Alg. 1 line 1). */
 int dg_engine_fill_synthetic(dg_engine* e, int which, uint64_t seed, uint32_t purpose,
                              int per_node, uint64_t iteration);
+/* Consensus error of the current models over ALL nodes (collective: every rank
+ * calls it; synchronous).  *dispersion = sum_i ||x_i - xbar||^2 with
+ * xbar = (1/N) sum_i x_i (fp64 column sums, NCCL all-reduce across ranks);
+ * *mean_sq = ||xbar||^2.  gossip_consensus's error[t] (topology.hpp:90-96) is
+ * dispersion_t / dispersion_0. */
+int dg_engine_consensus(dg_engine* e, double* dispersion, double* mean_sq);
 /* One fused gossip + Adam step for iteration t (>= 1); asynchronous. */
 int dg_engine_step(dg_engine* e, long t);
 /* Waits for all queued work; DG_DIVERGENCE (with iteration) if any step

@@ -26,7 +26,7 @@ __all__ = [
     "make_one_peer_exponential", "make_aer", "make_static_exponential", "from_matrices",
     "validate", "spectral_lambda", "effective_lambda", "OptimizerConfig", "gossip_mix",
     "dadam_step", "accum_adam_step", "check_divergence", "fill_synthetic", "Engine",
-    "nccl_unique_id", "plan_exchange", "library_path", "DADAM", "ACCUM",
+    "nccl_unique_id", "plan_exchange", "library_path", "DADAM", "ACCUM", "gossip_consensus",
     "TRANSPORT_AUTO", "TRANSPORT_NCCL", "TRANSPORT_P2P",
     "X", "G", "M", "V", "ACC", "Stream",
 ]
@@ -142,6 +142,7 @@ SIGNATURES = {
     "dg_engine_download": ([_VP, _I, _I, _VP, _SZ, _SZ], _I),
     "dg_engine_fill_synthetic": ([_VP, _I, C.c_uint64, C.c_uint32, _I, C.c_uint64], _I),
     "dg_engine_gather": ([_VP, _I, _I, _VP, _SZ, _VP], _I),
+    "dg_engine_consensus": ([_VP, _DP, _DP], _I),
     "dg_engine_step": ([_VP, _L], _I),
     "dg_engine_sync": ([_VP], _I),
     "dg_engine_streams": ([_VP, C.POINTER(_VP), C.POINTER(_VP)], _I),
@@ -403,6 +404,37 @@ def fill_synthetic(out, seed: int, purpose: int, worker: int, iteration: int, st
                                        iteration, _stream(stream)))
 
 
+# ----------------------------------------------------------------------------- consensus (f2)
+def gossip_consensus(schedule: MixingSchedule, x0: np.ndarray, rounds: int, device: int = 0) -> np.ndarray:
+    """gossip_consensus (topology.hpp:90-100) on one GPU:
+    x <- W^(t) x for t = 1..rounds on fp32 buckets (fp64 mixing accumulation),
+    error[t] = sum_i ||x_i - xbar||^2 / sum_i ||x_i^0 - xbar||^2; zero initial
+    dispersion gives an all-zero trajectory.  The step is the fused engine with
+    zero gradients, where DAdam reduces exactly to x <- mix."""
+    x0 = np.ascontiguousarray(x0, np.float32)
+    n, d = x0.shape
+    if n != schedule.workers():
+        raise ConfigError("gossip_consensus: x0 size mismatch")
+    if rounds < 0:
+        raise ConfigError("gossip_consensus: rounds < 0")
+    eng = Engine(schedule, d, OptimizerConfig(), device=device)
+    try:
+        for i in range(n):
+            eng.upload(i, X, x0[i])
+        err = np.zeros(rounds + 1)
+        d0, _ = eng.consensus()
+        if d0 == 0.0:
+            return err
+        err[0] = 1.0
+        for t in range(1, rounds + 1):
+            eng.step(t)
+            err[t] = eng.consensus()[0] / d0
+        eng.sync()
+        return err
+    finally:
+        eng.close()
+
+
 # ----------------------------------------------------------------------------- engine
 def nccl_unique_id() -> bytes:
     buf = (C.c_char * 128)()
@@ -462,6 +494,12 @@ class Engine:
         _check(lib().dg_engine_gather(self._h, local, which, idx.ctypes.data_as(_VP), idx.size,
                                       out.ctypes.data_as(_VP)))
         return out
+
+    def consensus(self):
+        """(sum_i ||x_i - xbar||^2, ||xbar||^2) over all nodes; collective across ranks."""
+        a, b = C.c_double(), C.c_double()
+        _check(lib().dg_engine_consensus(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def fill_synthetic(self, which: int, seed: int, purpose: int, per_node: bool, iteration: int):
         _check(lib().dg_engine_fill_synthetic(self._h, which, seed, purpose, int(per_node), iteration))

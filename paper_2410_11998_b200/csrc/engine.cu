@@ -824,6 +824,36 @@ int dg_engine_fill_synthetic(dg_engine* e, int which, uint64_t seed, uint32_t pu
   });
 }
 
+int dg_engine_consensus(dg_engine* e, double* dispersion, double* mean_sq) {
+  return guarded([&] {
+    if (!e) dg::config_error("engine_consensus: null handle");
+    CU(cudaSetDevice(e->device));
+    dg::NodePtrs xp{};
+    for (int i = 0; i < e->NL; ++i) xp.p[i] = e->buf(DG_BUF_X, i);
+    double* colsum = nullptr;
+    double* out = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&colsum), e->d * sizeof(double), e->comp));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&out), 2 * sizeof(double), e->comp));
+    CU(cudaMemsetAsync(out, 0, 2 * sizeof(double), e->comp));
+    const unsigned grid = dg::grid_for((long long)e->d, 8);
+    dg::column_sum<<<grid, 256, 0, e->comp>>>(colsum, xp, e->NL, (long long)e->d);
+    CU(cudaGetLastError());
+    if (e->G > 1) NC(ncclAllReduce(colsum, colsum, e->d, ncclDouble, ncclSum, e->nccl, e->comp));
+    // mean term counted once (rank 0); dispersion of the resident nodes on every rank
+    dg::dispersion<<<grid, 256, 0, e->comp>>>(out, colsum, 1.0 / double(e->N), xp, e->NL, (long long)e->d,
+                                              e->rank == 0);
+    CU(cudaGetLastError());
+    if (e->G > 1) NC(ncclAllReduce(out, out, 2, ncclDouble, ncclSum, e->nccl, e->comp));
+    double h[2];
+    CU(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, e->comp));
+    CU(cudaFreeAsync(colsum, e->comp));
+    CU(cudaFreeAsync(out, e->comp));
+    CU(cudaStreamSynchronize(e->comp));
+    if (dispersion) *dispersion = h[0];
+    if (mean_sq) *mean_sq = h[1];
+  });
+}
+
 int dg_engine_step(dg_engine* e, long t) {
   return guarded([&] {
     if (!e) dg::config_error("engine_step: null handle");

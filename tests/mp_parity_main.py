@@ -79,6 +79,13 @@ def main():
             keys = [("x", dg.X), ("m", dg.M), ("v", dg.V)] + ([("b", dg.ACC)] if algo else [])
             f = eng.first_node
             stats = eng.stats()
+            # f2: collective consensus error over all ranks vs the mirror's states
+            disp, msq = eng.consensus()
+            xb = st["x"].astype(np.float64).mean(0)
+            want_disp = float(((st["x"].astype(np.float64) - xb) ** 2).sum())
+            if abs(disp - want_disp) > 1e-9 * want_disp or abs(msq - float(xb @ xb)) > 1e-9 * float(xb @ xb):
+                print(f"rank {rank}: CONSENSUS MISMATCH {fn}{args} {disp} vs {want_disp}", flush=True)
+                bad += 1
             for k, w in keys:
                 got = np.stack([eng.download(i, w) for i in range(eng.local_nodes)])
                 want = st[k][f:f + eng.local_nodes]
