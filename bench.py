@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--d", type=int, default=125_000_000)
     p.add_argument("--topology", default="one_peer_exponential",
                    choices=["one_peer_exponential", "one_peer_ring", "static_exponential", "aer"])
-    p.add_argument("--algo", choices=["dadam", "accum"], default="dadam")
+    p.add_argument("--algo", choices=["dadam", "accum", "allreduce"], default="dadam")
     p.add_argument("--chunk", type=int, default=0)
     p.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
     p.add_argument("--e2e-steps", type=int, default=4)
@@ -73,7 +73,13 @@ def make_schedule(mod, topo, n):
 def hyper(algo):
     if algo == "dadam":
         return dict(alpha=2e-3, beta1=0.974, beta2=0.999, eps=1e-8, s=1)
+    if algo == "allreduce":
+        return dict(alpha=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, s=1)     # PAPER.md:1153 (All-Reduce Adam)
     return dict(alpha=8e-4, beta1=0.9, beta2=0.999, eps=1e-8, s=4)
+
+
+def algo_code(dg, algo):
+    return {"dadam": dg.DADAM, "accum": dg.ACCUM, "allreduce": dg.ALLREDUCE}[algo]
 
 
 def config_block(a, world, nodes):
@@ -151,7 +157,7 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def step_roofline(sched, world, d, steps_t, hbm_bw, transport, per_update=HBM_PER_UPDATE):
+def step_roofline(sched, world, d, steps_t, hbm_bw, transport, per_update=HBM_PER_UPDATE, algo="dadam"):
     """SURVEY.md 8(d) per-GPU step bound, summed over the timed rounds:
     max over GPUs of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL).
     NCCL transport: every received remote bucket costs 12 B/param of HBM (owner
@@ -160,6 +166,11 @@ def step_roofline(sched, world, d, steps_t, hbm_bw, transport, per_update=HBM_PE
     read (4 B/param per bucket served to a peer)."""
     import paper_2410_11998_b200 as dg
     n = sched.workers()
+    if algo == "allreduce":  # column sums (8 B/elem written + read) + ring all-reduce of fp64 sums
+        nl = -(-n // world)
+        t_hbm = d * (per_update * nl + 16.0) / hbm_bw
+        t_nvl = (2.0 * (world - 1) / world) * 8.0 * d / NVL_MEASURED if world > 1 else 0.0
+        return len(steps_t) * max(t_hbm, t_nvl)
     total = 0.0
     cache = {}
     for t in steps_t:
@@ -189,7 +200,7 @@ def cpu_reference_run(a, nodes_sample, d_sample, steps, threads):
     from oracle import pyoracle as O
     h = hyper(a.algo)
     cfg = O.OptimizerConfig(**h)
-    algo = O.DADAM if a.algo == "dadam" else O.ACCUM
+    algo = algo_code(O, a.algo)
     s = {"one_peer_exponential": O.make_one_peer_exponential, "one_peer_ring": O.make_one_peer_ring,
          "static_exponential": O.make_static_exponential}.get(a.topology, lambda n: O.make_aer(n, 2))(nodes_sample)
     st = O.init_state(nodes_sample, d_sample, SEED, True, np.float64, algo)
@@ -272,7 +283,7 @@ def run_ours(a):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     nodes = a.nodes_per_gpu * world
     sched = make_schedule(dg, a.topology, nodes)
-    algo = dg.DADAM if a.algo == "dadam" else dg.ACCUM
+    algo = algo_code(dg, a.algo)
     h = hyper(a.algo)
     total_t = a.warmup + a.steps + a.e2e_steps + 8
     total_t += (-total_t) % 4
@@ -284,7 +295,10 @@ def run_ours(a):
     eng = dg.Engine(sched, a.d, dg.OptimizerConfig(**h), algo=algo, total_steps=total_t, world_size=world,
                     rank=rank, device=local, nccl_id=nccl_id, chunk=a.chunk,
                     transport=dg.TRANSPORT_P2P if a.transport == "p2p" else dg.TRANSPORT_NCCL)
-    eng.fill_synthetic(dg.X, SEED, dg.Stream.CONSENSUS_INIT, True, 0)
+    if a.algo == "allreduce":   # All-Reduce Adam: workers share x^(0) (Alg. 2 line 1)
+        eng.fill_synthetic(dg.X, SEED, dg.Stream.INIT_MODEL, False, 0)
+    else:                        # dispersed models so mixing is exercised from step 1
+        eng.fill_synthetic(dg.X, SEED, dg.Stream.CONSENSUS_INIT, True, 0)
     eng.fill_synthetic(dg.G, SEED, dg.Stream.MINIBATCH, True, 1)
     eng.sync()
     comp_ptr, _ = eng.streams()
@@ -342,7 +356,7 @@ def run_ours(a):
     achieved = st["timed_hbm_bytes"] / kern_s if kern_s > 0 else 0.0
     per_launch = st["timed_hbm_bytes"] / max(1, st["timed_launches"])
     transport = "p2p" if st["transport"] == dg.TRANSPORT_P2P else "nccl"
-    roof_step_s = step_roofline(sched, world, a.d, timed_t, hbm_bw, transport)
+    roof_step_s = step_roofline(sched, world, a.d, timed_t, hbm_bw, transport, algo=a.algo)
 
     # ---- end to end through the public API: pinned host g -> H2D each step, step, D2H status
     e2e = None

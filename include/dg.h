@@ -137,7 +137,12 @@ int dg_fill_synthetic_f32(float* out, size_t n, uint64_t seed, uint32_t purpose,
  * for the hot path.
  * ====================================================================== */
 typedef struct dg_engine dg_engine;
-enum { DG_ALGO_DADAM = 0, DG_ALGO_ACCUM = 1 };
+/* DG_ALGO_ALLREDUCE: All-Reduce Adam (Alg. 2),
+ * the comparison baseline: gbar = mean of all N nodes'
+ * gradients (fp64 column sums, NCCL all-reduce across ranks), every node applies
+ * Adam with gbar and no mixing; nodes must stay identical (|x_i - x_0| <= 1e-12,
+ * else dg_engine_sync returns DG_INVARIANT).  The schedule only fixes N. */
+enum { DG_ALGO_DADAM = 0, DG_ALGO_ACCUM = 1, DG_ALGO_ALLREDUCE = 2 };
 enum { DG_BUF_X = 0, DG_BUF_G = 1, DG_BUF_M = 2, DG_BUF_V = 3, DG_BUF_ACC = 4 };
 
 typedef struct dg_engine_config {

@@ -374,6 +374,46 @@ void set_threads(int threads) {
 #endif
 }
 
+// All-Reduce Adam step (Alg. 2): gbar =
+// mean_of(g_1..g_N) (vec.cpp:59-69: ascending sum in double, then * 1/N),
+// every worker applies Adam with gbar and no mixing (x + (-alpha) * dir).
+// Workers must hold identical states (max |x_i - x_0| <= 1e-12) -> else InvariantError.
+template <class T>
+int allreduce_step(const or_sched* s, size_t d, long t, uint64_t seed, bool gen_grad, const T* gin, T* x,
+                   T* m, T* v, const TS<T>& ts) {
+  const int n = s->workers;
+  for (int i = 1; i < n; ++i)
+    for (size_t e = 0; e < d; ++e)
+      if (std::fabs(double(x[size_t(i) * d + e]) - double(x[e])) > 1e-12)
+        return fail(OR_INVARIANT, "allreduce_adam_step: worker states diverged");
+  std::vector<double> acc(d, 0.0);
+  std::vector<T> g(d), gbar(d);
+  for (int i = 0; i < n; ++i) {
+    const T* gi = gin ? gin + size_t(i) * d : nullptr;
+    if (gen_grad) {
+      const uint64_t st = stream_state(seed, 2u, uint64_t(i), uint64_t(t));
+      for (size_t e = 0; e < d; ++e) g[e] = T(bucket_value(draw(st, e)));
+      gi = g.data();
+    }
+    for (size_t e = 0; e < d; ++e) acc[e] = acc[e] + double(gi[e]);
+  }
+  const double inv = 1.0 / double(n);
+  for (size_t e = 0; e < d; ++e) gbar[e] = T(acc[e] * inv);
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+  for (int i = 0; i < n; ++i) {
+    const size_t o = size_t(i) * d;
+    std::vector<T> self(x + o, x + o + d);  // "mixing" with W = I: x_i itself
+    dadam_elems(x + o, gbar.data(), m + o, v + o, self.data(), d, ts);
+    if (!all_finite(x + o, d) || !all_finite(m + o, d) || !all_finite(v + o, d)) bad = 1;
+  }
+  if (bad) {
+    g_div_iter = t;
+    return fail(OR_DIVERGENCE, "non-finite state at iteration " + std::to_string(t));
+  }
+  return OR_OK;
+}
+
 // One Jacobi step for all nodes (parallel_for over workers, parallel.hpp:13-23;
 // snapshot semantics SPEC.md:317). gen_grad: draw g_i^(t) from the Minibatch stream.
 template <class T>
@@ -389,6 +429,7 @@ int step_all(const or_sched* s, int algo, const or_adam_cfg* cfg, size_t d, long
   std::memcpy(xprev, x, sizeof(T) * size_t(n) * d);
   const bool fold = algo == OR_ACCUM && (t % cfg->s == 0);
   int bad = 0;
+  if (algo == OR_ALLREDUCE) return allreduce_step<T>(s, d, t, seed, gen_grad, gin, x, m, v, ts);
 #pragma omp parallel for schedule(static) reduction(| : bad)
   for (int i = 0; i < n; ++i) {
     std::vector<T> mixed(d), gbuf;

@@ -93,7 +93,7 @@ int or_accum_adam_step_f32(float* x, const float* g, float* m_hat, float* v_hat,
  * snapshot of x^(t-1), gradients g_i^(t)[e] = (float)(2u-1) from
  * StreamRng(seed, Minibatch=2, i, t).  algo: 0 = DAdam, 1 = AccumAdam.
  * States are n x d row-major.  b may be NULL for DAdam.  */
-enum { OR_DADAM = 0, OR_ACCUM = 1 };
+enum { OR_DADAM = 0, OR_ACCUM = 1, OR_ALLREDUCE = 2 /* Alg. 2 */ };
 int or_run_f64(const or_sched* s, int algo, const or_adam_cfg* cfg, uint64_t seed, size_t d,
                long t_begin, long t_end, long T, int threads, double* x, double* m, double* v,
                double* b);

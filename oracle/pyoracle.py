@@ -19,7 +19,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 OK, CONFIG_ERROR, DIVERGENCE, INVARIANT = 0, 2, 3, 4
 COMPLETE, ONE_PEER_RING, ONE_PEER_EXP, AER, STATIC_EXP = range(5)
-DADAM, ACCUM = 0, 1
+DADAM, ACCUM, ALLREDUCE = 0, 1, 2
 # rng.hpp:9-16
 DATASET, MINIBATCH, SPEED_NOISE, INIT_MODEL, TAU_SAMPLE, CONSENSUS_INIT = 1, 2, 3, 4, 5, 6
 

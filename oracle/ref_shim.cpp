@@ -99,6 +99,33 @@ int ref_run(int algo, int n, size_t d, int period, int maxdeg, const int* nbr_id
       const int r = int((t - 1) % period);
       const std::vector<Vec> Xprev = X;  // Jacobi snapshot
       std::vector<int> bad(n, 0);
+      if (algo == 2) {  // All-Reduce Adam: gbar = mean_of(g), no mixing
+        std::vector<Vec> Gt(n);
+        for (int i = 0; i < n; ++i) {
+          if (gen_grad) {
+            StreamRng rng(seed, Stream::Minibatch, uint64_t(i), uint64_t(t));
+            Gt[i].resize(d);
+            for (size_t e = 0; e < d; ++e) Gt[i][e] = double(static_cast<float>(2.0 * rng.next_unit() - 1.0));
+          } else {
+            Gt[i] = G[i];
+          }
+        }
+        const Vec gbar = mean_of(Gt);
+        for (int i = 1; i < n; ++i)
+          if (linf_norm(sub(X[i], X[0])) > 1e-12) throw InvariantError("allreduce_adam_step: workers diverged");
+        parallel_for(Exec::OpenMP, n, [&](int i) {
+          M[i] = add(scale(M[i], cfg->beta1), scale(gbar, 1.0 - cfg->beta1));
+          V[i] = add(scale(V[i], cfg->beta2), scale(hadamard_square(gbar), 1.0 - cfg->beta2));
+          const Vec dir = div_by_sqrt_plus_eps(scale(M[i], c1), scale(V[i], c2), cfg->eps);
+          Vec xn = Xprev[i];
+          axpy(-cfg->alpha, dir, xn);
+          X[i] = std::move(xn);
+          bad[i] = !(all_finite(X[i]) && all_finite(M[i]) && all_finite(V[i]));
+        });
+        for (int i = 0; i < n; ++i)
+          if (bad[i]) throw DivergenceError(t, "non-finite state at iteration " + std::to_string(t));
+        continue;
+      }
       parallel_for(Exec::OpenMP, n, [&](int i) {
         Vec g;
         if (gen_grad) {

@@ -26,7 +26,7 @@ __all__ = [
     "make_one_peer_exponential", "make_aer", "make_static_exponential", "from_matrices",
     "validate", "spectral_lambda", "effective_lambda", "OptimizerConfig", "gossip_mix",
     "dadam_step", "accum_adam_step", "check_divergence", "fill_synthetic", "Engine",
-    "nccl_unique_id", "plan_exchange", "library_path", "DADAM", "ACCUM", "gossip_consensus",
+    "nccl_unique_id", "plan_exchange", "library_path", "DADAM", "ACCUM", "ALLREDUCE", "gossip_consensus",
     "TRANSPORT_AUTO", "TRANSPORT_NCCL", "TRANSPORT_P2P",
     "X", "G", "M", "V", "ACC", "Stream",
 ]
@@ -35,7 +35,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # DG_LIB overrides the library path (kernel-variant sweeps, scripts/sweep.py).
 _LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg.so")
 
-DADAM, ACCUM = 0, 1
+DADAM, ACCUM, ALLREDUCE = 0, 1, 2
 TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_P2P = 0, 1, 2
 X, G, M, V, ACC = 0, 1, 2, 3, 4
 

@@ -65,7 +65,7 @@ DevScalars scalars(const dg_adam_cfg* cin, int algo, long t, long T, bool* fold)
     if (T < 1 || T % c->s) config_error("accum_adam_step: T mod s != 0");
     if (t > T) config_error("accum_adam_step: t exceeds T");
     tau = (t + c->s - 1) / c->s;
-  } else if (algo != DG_ALGO_DADAM) {
+  } else if (algo != DG_ALGO_DADAM && algo != DG_ALGO_ALLREDUCE) {
     config_error("unknown algorithm");
   }
   if (fold) *fold = algo == DG_ALGO_ACCUM && t % c->s == 0;
@@ -421,6 +421,13 @@ struct dg_engine {
   double kernel_ms = 0, timed_bytes = 0;
   long timed_launches = 0;
   void harvest_timing();
+  // times (optionally) and counts one launch of ours on the compute stream
+  template <class F>
+  void timed(double bytes, F&& launch);
+  // All-Reduce Adam (f3)
+  double* gsum = nullptr;  // [d_pad] fp64 gradient column sums
+  int* inv_flag = nullptr; // first iteration with drifting workers (INT_MAX = none)
+  void step_allreduce(long t, const dg::DevScalars& s);
 
   float* x_alt = nullptr;  // second x buffer (ping-pong rounds)
   int xcur = 0;            // which x buffer holds the current x (identical on every rank)
@@ -467,6 +474,8 @@ dg_engine::~dg_engine() {
     for (int r = 0; r < int(peer_base[b].size()); ++r)
       if (r != rank && peer_base[b][r]) cudaIpcCloseMemHandle(peer_base[b][r]);
   if (flag) cudaFree(flag);
+  if (inv_flag) cudaFree(inv_flag);
+  if (gsum) cudaFree(gsum);
   if (ev_begin) cudaEventDestroy(ev_begin);
   for (auto e : ev_slot_free)
     if (e) cudaEventDestroy(e);
@@ -530,6 +539,50 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   hbm += bytes;
 }
 
+template <class F>
+void dg_engine::timed(double bytes, F&& launch) {
+  if (timing) {
+    if (tev_used == tev.size()) {
+      cudaEvent_t a, b;
+      CU(cudaEventCreate(&a));
+      CU(cudaEventCreate(&b));
+      tev.push_back({a, b});
+      tev_bytes.push_back(0);
+    }
+    CU(cudaEventRecord(tev[tev_used].first, comp));
+  }
+  launch();
+  dg::cuda_check(cudaGetLastError(), "kernel launch");
+  if (timing) {
+    CU(cudaEventRecord(tev[tev_used].second, comp));
+    tev_bytes[tev_used++] = bytes;
+  }
+  ++launches;
+  hbm += bytes;
+}
+
+void dg_engine::step_allreduce(long t, const dg::DevScalars& s) {
+  dg::NodePtrs g{};
+  dg::NodeMutPtrs x{}, m{}, v{};
+  for (int i = 0; i < NL; ++i) {
+    g.p[i] = buf(DG_BUF_G, i);
+    x.p[i] = buf(DG_BUF_X, i);
+    m.p[i] = buf(DG_BUF_M, i);
+    v.p[i] = buf(DG_BUF_V, i);
+  }
+  const unsigned grid = dg::grid_for((long long)d, 8);
+  // column sums of the resident gradients: read NL x 4 B, write 8 B per element
+  timed(double(d) * (4.0 * NL + 8.0), [&] {
+    dg::column_sum<<<grid, 256, 0, comp>>>(gsum, g, NL, (long long)d);
+  });
+  if (G > 1) NC(ncclAllReduce(gsum, gsum, d, ncclDouble, ncclSum, nccl, comp));  // the All-Reduce
+  // update: read gsum 8 B + x, m, v; write x, m, v
+  timed(double(d) * (24.0 * NL + 8.0), [&] {
+    dg::allreduce_adam<<<grid, 256, 0, comp>>>(x, m, v, NL, gsum, 1.0 / double(N), (long long)d, s, int(t), flag,
+                                               inv_flag);
+  });
+}
+
 void dg_engine::harvest_timing() {
   for (size_t k = 0; k < tev_used; ++k) {
     float ms = 0;
@@ -548,6 +601,7 @@ void dg_engine::step(long t) {
   const size_t ri = size_t((t - 1) % P);
   const dg::RoundPlan& p = plans[ri];
   ++steps;
+  if (algo == DG_ALGO_ALLREDUCE) return step_allreduce(t, s);
   if (transport == DG_TRANSPORT_P2P && G > 1) {
     // Cross-GPU step barrier, stream-ordered on the compute stream, before any
     // step that reads peers' x^(t-1) (their step t-1 must be complete) and
@@ -650,7 +704,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       e->transport = std::string(tr) == "nccl" ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
       auto_transport = false;
     }
-    bool p2p = e->transport == DG_TRANSPORT_P2P && e->G > 1;
+    bool p2p = e->transport == DG_TRANSPORT_P2P && e->G > 1 && c->algo != DG_ALGO_ALLREDUCE;
     // x double-buffered ("ping-pong") rounds: mixing components of >=
     // DG_PINGPONG_MIN_NC members (default 4) anywhere, and with the P2P transport
     // every round in which any rank reads a remote bucket.  Decided from the
@@ -696,8 +750,11 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     }
     if (e->max_recv && !p2p) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
     CU(cudaMalloc(&e->flag, sizeof(int)));
+    CU(cudaMalloc(&e->inv_flag, sizeof(int)));
     const int none = INT_MAX;
     CU(cudaMemcpyAsync(e->flag, &none, sizeof(int), cudaMemcpyHostToDevice, e->comp));
+    CU(cudaMemcpyAsync(e->inv_flag, &none, sizeof(int), cudaMemcpyHostToDevice, e->comp));
+    if (c->algo == DG_ALGO_ALLREDUCE) CU(cudaMalloc(&e->gsum, sizeof(double) * e->d_pad));
     CU(cudaStreamSynchronize(e->comp));
     if (e->G > 1) {
       ncclUniqueId id;
@@ -877,6 +934,10 @@ int dg_engine_sync(dg_engine* e) {
     CU(cudaMemcpy(&f, e->flag, sizeof(int), cudaMemcpyDeviceToHost));
     if (f != INT_MAX)
       throw dg::Error(DG_DIVERGENCE, "non-finite state at iteration " + std::to_string(f), f);
+    int inv = INT_MAX;
+    CU(cudaMemcpy(&inv, e->inv_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (inv != INT_MAX)
+      throw dg::Error(DG_INVARIANT, "allreduce_adam_step: worker states diverged at iteration " + std::to_string(inv));
   });
 }
 

@@ -97,6 +97,28 @@ def main():
                   f"barriers {stats['barriers']}", flush=True)
             eng.close()
             dist.barrier()
+    # f3: All-Reduce Adam across ranks (NCCL all-reduce of fp64 gradient column sums)
+    for n_nodes in (8, 16):
+        obj = [dg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        acfg = dict(alpha=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, s=1)
+        eng = dg.Engine(dg.make_complete(n_nodes), d, dg.OptimizerConfig(**acfg), algo=dg.ALLREDUCE, total_steps=T,
+                        world_size=world, rank=rank, device=local, nccl_id=obj[0], transport=TRANSPORT)
+        eng.fill_synthetic(dg.X, SEED, dg.Stream.INIT_MODEL, False, 0)
+        for t in range(1, T + 1):
+            eng.fill_synthetic(dg.G, SEED, dg.Stream.MINIBATCH, True, t)
+            eng.step(t)
+        eng.sync()
+        st = O.init_state(n_nodes, d, SEED, False, np.float32)
+        O.run(O.make_complete(n_nodes), O.ALLREDUCE, O.OptimizerConfig(**acfg), SEED, st, 1, T)
+        f = eng.first_node
+        for k, w in (("x", dg.X), ("m", dg.M), ("v", dg.V)):
+            got = np.stack([eng.download(i, w) for i in range(eng.local_nodes)])
+            if not np.array_equal(got.view(np.uint32), st[k][f:f + eng.local_nodes].view(np.uint32)):
+                print(f"rank {rank}: MISMATCH allreduce n={n_nodes} {k}", flush=True)
+                bad += 1
+        eng.close()
+        dist.barrier()
     dist.destroy_process_group()
     print(f"rank {rank}: {'ok' if not bad else f'{bad} mismatches'}", flush=True)
     sys.exit(1 if bad else 0)
