@@ -157,7 +157,14 @@ typedef struct dg_engine_config {
   dg_adam_cfg adam;
   long total_steps;            /* T (AccumAdam requires T mod s == 0) */
   int transport;               /* DG_TRANSPORT_*: how remote neighbour buckets move (world_size > 1) */
+  int flags;                   /* DG_ENGINE_* */
 } dg_engine_config;
+
+/* DG_ENGINE_IN_PLACE: x is never double-buffered (the DG_BUF_X pointer is
+ * stable for the engine's lifetime, e.g. framework parameters are views of
+ * it); forces the NCCL transport when world_size > 1.  Required for
+ * dg_engine_step_range. */
+enum { DG_ENGINE_IN_PLACE = 1 };
 
 /* DG_TRANSPORT_P2P (default): the fused kernel reads remote neighbours'
  * x^(t-1) directly from peer HBM over NVLink (CUDA IPC mappings; x is
@@ -215,6 +222,22 @@ int dg_engine_fill_synthetic(dg_engine* e, int which, uint64_t seed, uint32_t pu
 int dg_engine_consensus(dg_engine* e, double* dispersion, double* mean_sq);
 /* One fused gossip + Adam step for iteration t (>= 1); asynchronous. */
 int dg_engine_step(dg_engine* e, long t);
+/* Bucketed step (the paper's per-bucket update U_k, PAPER.md:302-304 and
+ * 1089-1095).  Updates elements [off, off+len) of every
+ * resident node for iteration t -- mixing with round-t peers, Adam -- after
+ * the round-t exchange of that range (pre-posted by the same range's call at
+ * t-1, else posted now) has landed, then immediately posts the round-(t+1)
+ * exchange of the updated range on the comm stream so it overlaps whatever
+ * the caller does next (the rest of backward, the next forward).  Every rank
+ * must call the same ranges in the same order; off must be a multiple of 64;
+ * the ranges of one iteration must tile [0, d).  Requires DG_ENGINE_IN_PLACE. */
+int dg_engine_step_range(dg_engine* e, long t, size_t off, size_t len);
+/* Stream joins with a caller stream (cudaStream_t): wait_stream makes the
+ * engine's streams wait for work already queued on `stream` (e.g. backward
+ * producing g); join makes `stream` wait for the engine's queued updates
+ * (e.g. the next forward reading x). */
+int dg_engine_wait_stream(dg_engine* e, void* stream);
+int dg_engine_join(dg_engine* e, void* stream);
 /* Waits for all queued work; DG_DIVERGENCE (with iteration) if any step
  * produced a non-finite state; DG_NCCL_ERROR on an asynchronous NCCL error. */
 int dg_engine_sync(dg_engine* e);

@@ -37,6 +37,7 @@ _LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg.so")
 
 DADAM, ACCUM, ALLREDUCE = 0, 1, 2
 TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_P2P = 0, 1, 2
+ENGINE_IN_PLACE = 1
 X, G, M, V, ACC = 0, 1, 2, 3, 4
 
 
@@ -94,7 +95,7 @@ class _EngineConfig(C.Structure):
     _fields_ = [("schedule", C.c_void_p), ("world_size", C.c_int), ("rank", C.c_int),
                 ("device", C.c_int), ("nccl_id", C.c_void_p), ("d", C.c_size_t),
                 ("chunk", C.c_size_t), ("algo", C.c_int), ("adam", _AdamCfg),
-                ("total_steps", C.c_long), ("transport", C.c_int)]
+                ("total_steps", C.c_long), ("transport", C.c_int), ("flags", C.c_int)]
 
 
 class _EngineStats(C.Structure):
@@ -149,6 +150,9 @@ SIGNATURES = {
     "dg_engine_get_stats": ([_VP, C.POINTER(_EngineStats)], _I),
     "dg_engine_destroy": ([_VP], None),
     "dg_engine_set_timing": ([_VP, _I], _I),
+    "dg_engine_step_range": ([_VP, _L, _SZ, _SZ], _I),
+    "dg_engine_wait_stream": ([_VP, _VP], _I),
+    "dg_engine_join": ([_VP, _VP], _I),
     "dg_plan_exchange": ([_VP, _I, _I, _L, _IP, _IP, _IP, _IP, _IP, _IP, _I], _I),
 }
 
@@ -447,14 +451,15 @@ class Engine:
 
     def __init__(self, schedule: MixingSchedule, d: int, cfg: OptimizerConfig, algo: int = DADAM,
                  total_steps: int = 0, world_size: int = 1, rank: int = 0, device: int = 0,
-                 nccl_id: Optional[bytes] = None, chunk: int = 0, transport: int = TRANSPORT_AUTO):
+                 nccl_id: Optional[bytes] = None, chunk: int = 0, transport: int = TRANSPORT_AUTO,
+                 flags: int = 0):
         self.schedule = schedule
         idbuf = None
         if nccl_id is not None:
             idbuf = (C.c_char * 128).from_buffer_copy(nccl_id)
         ec = _EngineConfig(schedule.handle.value, world_size, rank, device,
                            C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
-                           d, chunk, algo, cfg._c(), total_steps, transport)
+                           d, chunk, algo, cfg._c(), total_steps, transport, flags)
         h = C.c_void_p()
         _check(lib().dg_engine_create(C.byref(ec), C.byref(h)))
         self._h = h
@@ -506,6 +511,15 @@ class Engine:
 
     def step(self, t: int):
         _check(lib().dg_engine_step(self._h, t))
+
+    def step_range(self, t: int, off: int, length: int):
+        _check(lib().dg_engine_step_range(self._h, t, off, length))
+
+    def wait_stream(self, stream):
+        _check(lib().dg_engine_wait_stream(self._h, _stream(stream)))
+
+    def join(self, stream):
+        _check(lib().dg_engine_join(self._h, _stream(stream)))
 
     def sync(self):
         _check(lib().dg_engine_sync(self._h))

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 
@@ -424,6 +425,14 @@ struct dg_engine {
   // times (optionally) and counts one launch of ours on the compute stream
   template <class F>
   void timed(double bytes, F&& launch);
+  // bucketed steps (f1)
+  bool in_place = false;
+  float* rbuf = nullptr;                     // [max_recv][d_pad] recv buffers for step_range
+  std::map<size_t, cudaEvent_t> range_ev;   // exchange-complete event per range offset
+  std::map<size_t, long> range_posted;      // iteration whose exchange is posted per range
+  cudaEvent_t ev_user = nullptr;
+  void post_range_exchange(const dg::RoundPlan& q, size_t off, size_t len);
+  void step_range(long t, size_t off, size_t len);
   // All-Reduce Adam (f3)
   double* gsum = nullptr;  // [d_pad] fp64 gradient column sums
   int* inv_flag = nullptr; // first iteration with drifting workers (INT_MAX = none)
@@ -455,7 +464,7 @@ struct dg_engine {
     return std::max(1, comm ? sm_total - reserve_sms : sm_total);
   }
   void enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
-                     const dg::DevScalars& s, bool fold, long t);
+                     const dg::DevScalars& s, bool fold, long t, const float* const* slot_override = nullptr);
   void step(long t);
   ~dg_engine();
 };
@@ -476,6 +485,10 @@ dg_engine::~dg_engine() {
   if (flag) cudaFree(flag);
   if (inv_flag) cudaFree(inv_flag);
   if (gsum) cudaFree(gsum);
+  if (rbuf) cudaFree(rbuf);
+  for (auto& kv : range_ev)
+    if (kv.second) cudaEventDestroy(kv.second);
+  if (ev_user) cudaEventDestroy(ev_user);
   if (ev_begin) cudaEventDestroy(ev_begin);
   for (auto e : ev_slot_free)
     if (e) cudaEventDestroy(e);
@@ -489,7 +502,7 @@ dg_engine::~dg_engine() {
 }
 
 void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
-                              const dg::DevScalars& s, bool fold, long t) {
+                              const dg::DevScalars& s, bool fold, long t, const float* const* slot_override) {
   float *x[dg::kMaxLocal], *xo[dg::kMaxLocal], *m[dg::kMaxLocal], *v[dg::kMaxLocal], *b[dg::kMaxLocal];
   const float* g[dg::kMaxLocal];
   for (int i = 0; i < NL; ++i) {
@@ -502,8 +515,9 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   }
   const float* slot_ptr[dg::kMaxRemote];
   for (int r = 0; r < int(p.recv_node.size()); ++r)
-    slot_ptr[r] = transport == DG_TRANSPORT_P2P ? peer_x(p.recv_node[r]) + off
-                                                : slots + (size_t(slot_set) * max_recv + r) * chunk;
+    slot_ptr[r] = slot_override                  ? slot_override[r]
+                  : transport == DG_TRANSPORT_P2P ? peer_x(p.recv_node[r]) + off
+                                                  : slots + (size_t(slot_set) * max_recv + r) * chunk;
   const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr};
   const bool tma = dg::use_tma(p);
   LaunchFnHolder fnh{nullptr};
@@ -594,7 +608,59 @@ void dg_engine::harvest_timing() {
   tev_used = 0;
 }
 
+void dg_engine::post_range_exchange(const dg::RoundPlan& q, size_t off, size_t len) {
+  NC(ncclGroupStart());
+  for (size_t k = 0; k < q.send_node.size(); ++k)
+    NC(ncclSend(buf(DG_BUF_X, q.send_node[k] - first) + off, len, ncclFloat, q.send_peer[k], nccl, comm));
+  for (size_t r = 0; r < q.recv_node.size(); ++r)
+    NC(ncclRecv(rbuf + r * d_pad + off, len, ncclFloat, q.recv_peer[r], nccl, comm));
+  NC(ncclGroupEnd());
+  cudaEvent_t& ev = range_ev[off];
+  if (!ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CU(cudaEventRecord(ev, comm));
+  sent += 4.0 * double(len) * double(q.send_node.size());
+  received += 4.0 * double(len) * double(q.recv_node.size());
+}
+
+// U_k of the paper: wait for this range's round-t exchange (posted at t-1 or
+// now), update the range, post its round-(t+1) exchange.
+void dg_engine::step_range(long t, size_t off, size_t len) {
+  if (!in_place) dg::config_error("step_range: engine was not created with DG_ENGINE_IN_PLACE");
+  if (algo == DG_ALGO_ALLREDUCE) dg::config_error("step_range: not available for All-Reduce Adam");
+  if (off % dg::kAlign || off >= d || len == 0 || len > d - off)
+    dg::config_error("step_range: range must start at a multiple of 64 and lie inside [0, d)");
+  bool fold = false;
+  const dg::DevScalars s = dg::scalars(&adam, algo, t, T, &fold);
+  CU(cudaSetDevice(device));
+  const dg::RoundPlan& p = plans[size_t((t - 1) % P)];
+  const bool comm_now = G > 1 && !(p.send_node.empty() && p.recv_node.empty());
+  if (comm_now && !rbuf) CU(cudaMalloc(&rbuf, sizeof(float) * std::max(1, max_recv) * d_pad));
+  std::vector<const float*> slot_ptr(std::max<size_t>(1, p.recv_node.size()));
+  if (comm_now) {
+    auto it = range_posted.find(off);
+    if (it == range_posted.end() || it->second != t) {  // not pre-posted: exchange x^(t-1) now
+      CU(cudaEventRecord(ev_begin, comp));
+      CU(cudaStreamWaitEvent(comm, ev_begin, 0));
+      post_range_exchange(p, off, len);
+    }
+    CU(cudaStreamWaitEvent(comp, range_ev[off], 0));
+    for (size_t r = 0; r < p.recv_node.size(); ++r) slot_ptr[r] = rbuf + r * d_pad + off;
+  }
+  enqueue_fused(p, off, len, 0, s, fold, t, comm_now ? slot_ptr.data() : nullptr);
+  range_posted.erase(off);
+  const dg::RoundPlan& q = plans[size_t(t % P)];
+  if (G > 1 && !(q.send_node.empty() && q.recv_node.empty())) {
+    if (!rbuf) CU(cudaMalloc(&rbuf, sizeof(float) * std::max(1, max_recv) * d_pad));
+    CU(cudaEventRecord(ev_begin, comp));  // x^(t)[off, off+len) final
+    CU(cudaStreamWaitEvent(comm, ev_begin, 0));
+    post_range_exchange(q, off, len);     // C_k for iteration t+1, overlaps the caller's next work
+    range_posted[off] = t + 1;
+  }
+}
+
 void dg_engine::step(long t) {
+  if (!range_posted.empty())
+    dg::config_error("step: bucketed exchanges are in flight (use dg_engine_step_range consistently)");
   bool fold = false;
   const dg::DevScalars s = dg::scalars(&adam, algo, t, T, &fold);
   CU(cudaSetDevice(device));
@@ -698,9 +764,10 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       e->max_recv = std::max(e->max_recv, int(e->plans.back().recv_node.size()));
     }
     e->NL = e->plans[0].n_local;
-    e->transport = c->transport == DG_TRANSPORT_NCCL ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
+    e->in_place = (c->flags & DG_ENGINE_IN_PLACE) != 0;
+    e->transport = (c->transport == DG_TRANSPORT_NCCL || e->in_place) ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
     bool auto_transport = c->transport == DG_TRANSPORT_AUTO;
-    if (const char* tr = std::getenv("DG_TRANSPORT")) {
+    if (const char* tr = e->in_place ? nullptr : std::getenv("DG_TRANSPORT")) {
       e->transport = std::string(tr) == "nccl" ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
       auto_transport = false;
     }
@@ -710,7 +777,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     // every round in which any rank reads a remote bucket.  Decided from the
     // global schedule so that every rank flips its x buffer identically.
     const char* ppenv = std::getenv("DG_PINGPONG_MIN_NC");
-    const int pp_min = ppenv ? std::atoi(ppenv) : 4;
+    const int pp_min = e->in_place ? 0 : (ppenv ? std::atoi(ppenv) : 4);
     bool any_pp = false;
     e->round_remote.assign(e->P, 0);
     for (int r = 0; r < e->P; ++r) {
@@ -736,6 +803,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     CU(cudaStreamCreateWithFlags(&e->comp, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithPriority(&e->comm, cudaStreamNonBlocking, hi));  // comm first
     CU(cudaEventCreateWithFlags(&e->ev_begin, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&e->ev_user, cudaEventDisableTiming));
     for (auto& ev : e->ev_slot_free) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     e->ev_recv.resize(e->n_chunks);
     for (auto& ev : e->ev_recv) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -908,6 +976,31 @@ int dg_engine_consensus(dg_engine* e, double* dispersion, double* mean_sq) {
     CU(cudaStreamSynchronize(e->comp));
     if (dispersion) *dispersion = h[0];
     if (mean_sq) *mean_sq = h[1];
+  });
+}
+
+int dg_engine_step_range(dg_engine* e, long t, size_t off, size_t len) {
+  return guarded([&] {
+    if (!e) dg::config_error("engine_step_range: null handle");
+    e->step_range(t, off, len);
+  });
+}
+
+int dg_engine_wait_stream(dg_engine* e, void* stream) {
+  return guarded([&] {
+    if (!e) dg::config_error("engine_wait_stream: null handle");
+    CU(cudaSetDevice(e->device));
+    CU(cudaEventRecord(e->ev_user, static_cast<cudaStream_t>(stream)));
+    CU(cudaStreamWaitEvent(e->comp, e->ev_user, 0));
+  });
+}
+
+int dg_engine_join(dg_engine* e, void* stream) {
+  return guarded([&] {
+    if (!e) dg::config_error("engine_join: null handle");
+    CU(cudaSetDevice(e->device));
+    CU(cudaEventRecord(e->ev_user, e->comp));
+    CU(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), e->ev_user, 0));
   });
 }
 
