@@ -281,17 +281,9 @@ bool use_tma(const RoundPlan& p) {
   return m == 2 || (m == 1 && p.comp_size >= 4);
 }
 
-bool staged_bulk() {  // DG_STAGE_COPY: "tma" (bulk copies, default) or "async" (cp.async)
-  static const bool v = [] {
-    const char* e = std::getenv("DG_STAGE_COPY");
-    return !(e && std::string(e) == "async");
-  }();
-  return v;
-}
-
-template <int ALGO, bool FOLD, bool BULK, int NS>
-void launch_tma_b(const TmaArgs& a, size_t smem, long long units, cudaStream_t st) {
-  auto kern = gossip_adam_tma<ALGO, FOLD, BULK, NS>;
+template <int ALGO, bool FOLD, int NS>
+void launch_tma_n(const TmaArgs& a, size_t smem, long long units, cudaStream_t st) {
+  auto kern = gossip_adam_tma<ALGO, FOLD, NS>;
   static bool configured = false;
   if (!configured) {
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
@@ -303,13 +295,6 @@ void launch_tma_b(const TmaArgs& a, size_t smem, long long units, cudaStream_t s
   const long long resident = std::max(1LL, (long long)std::max(1, occ) * current_sms());
   const unsigned grid = unsigned(std::max(1LL, std::min(units, resident)));
   kern<<<grid, kTmaThreads, smem, st>>>(a);
-}
-template <int ALGO, bool FOLD, int NS>
-void launch_tma_n(const TmaArgs& a, size_t smem, long long units, cudaStream_t st) {
-  if (staged_bulk())
-    launch_tma_b<ALGO, FOLD, true, NS>(a, smem, units, st);
-  else
-    launch_tma_b<ALGO, FOLD, false, NS>(a, smem, units, st);
 }
 template <int ALGO, bool FOLD>
 void launch_tma_t(const TmaArgs& a, int ns_max, size_t smem, long long units, cudaStream_t st) {
@@ -366,7 +351,8 @@ void launch_tma(const RoundPlan& p, const Buffers& bf, int algo, bool fold, size
     nm_max = std::max(nm_max, a.nm[c]);
     ns_max = std::max(ns_max, a.ns[c]);
   }
-  int cols = kTmaThreads / std::min(nm_max, kTmaThreads) / 32 * 32;  // float4 columns per thread round
+  const int ct = kTmaConsumerWarps * 32;
+  int cols = ct / std::min(nm_max, ct) / 32 * 32;  // float4 columns per consumer-thread round
   cols = std::max(32, cols);
   const int max_cols = DG_TMA_STAGE_BYTES / (16 * rows_max);
   const int tile4 = max_cols >= cols ? max_cols / cols * cols : std::max(32, max_cols / 32 * 32);
@@ -374,7 +360,7 @@ void launch_tma(const RoundPlan& p, const Buffers& bf, int algo, bool fold, size
   a.rows_max = rows_max;
   a.t = t;
   a.div_flag = flag;
-  const size_t smem = 128 + size_t(DG_TMA_STAGES) * rows_max * a.tile * sizeof(float);
+  const size_t smem = 256 + size_t(DG_TMA_STAGES) * rows_max * a.tile * sizeof(float);
   const long long units = ((long long)len + a.tile - 1) / a.tile * a.n_comp;
   if (algo == DG_ALGO_DADAM)
     launch_tma_t<0, false>(a, ns_max, smem, units, st);

@@ -1,7 +1,6 @@
 cd $GRAFT_REPO_ROOT
-for args in "--topology static_exponential" "--topology aer --algo accum"; do
-  echo "== sweep $args"
-  for env in "DG_TMA=0 DG_COOP_MIN_NC=99" "DG_TMA=2" "DG_TMA=0"; do
-    echo "-- $env"; SWEEP_ENV="$env" timeout 900 python scripts/sweep.py $args 2>&1
-  done
+timeout 900 python -m pytest tests/test_gpu_kernel_paths.py -x -q -p no:cacheprovider 2>&1 | tail -2
+for args in "" "--topology static_exponential" "--topology aer --algo accum"; do
+  echo "== sweep TMA (ws) $args"
+  SWEEP_ENV="DG_TMA=2" timeout 900 python scripts/sweep.py $args 2>&1
 done
