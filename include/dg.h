@@ -251,6 +251,35 @@ int dg_engine_set_timing(dg_engine* e, int on);
 void dg_engine_destroy(dg_engine* e);
 
 /* ======================================================================
+ * Runtime model: the discrete-event
+ * per-iteration runtime recurrences of PAPER.md Appendix A.5 (All-Reduce and
+ * decentralized) and A.8.1 (SGP variant), evaluated
+ * verbatim; host only.  Unit time = one worker's forward pass with the global
+ * batch; forward 1/N (All-Reduce: b/N unless `normalized`), backward 2/N per
+ * bucket, theta per bucket update, gamma per bucket All-Reduce, omega*gamma per
+ * decentralized round, p^(i,t) ~ N(1, sigma2) truncated to [0.5, 1.5] drawn
+ * from StreamRng(seed, SpeedNoise, i, t) (rng.cpp:64-73).
+ * ====================================================================== */
+typedef struct dg_rm_params {
+  int N, b;                  /* workers, buckets */
+  double theta, gamma, omega, sigma2;
+  int workers_per_node;      /* SGP variant grouping (divides N) */
+  int normalized;            /* All-Reduce forward p/N instead of the paper-literal p*b/N */
+  int allow_omega_above_one;
+} dg_rm_params;
+enum { DG_RM_ALLREDUCE = 0, DG_RM_DECENTRALIZED = 1, DG_RM_SGP = 2 };
+/* runtimes[t-1] = max_i T_U^(i,t) - max_i T_U^(i,t-1) for t = 1..T.  schedule:
+ * neighbour sets N_i^(t) for DECENTRALIZED / SGP (NULL = complete).  timeline
+ * (optional): T x N x (1 + 3b) completion times F, B_1..B_b, U_1..U_b, C_1..C_b
+ * (All-Reduce stores its single U in U_1). */
+int dg_rm_simulate(int mode, const dg_rm_params* p, const dg_schedule* schedule, long T, uint64_t seed,
+                   double* runtimes, double* timeline);
+/* Eq. (3) best possible speedup */
+int dg_rm_closed_form_speedup(double gamma, int N, int b, double theta, double* out);
+/* p^(i,t) (rng.cpp:64-73 on StreamRng(seed, SpeedNoise, worker, iteration)) */
+int dg_rm_speed_multiplier(uint64_t seed, uint64_t worker, uint64_t iteration, double sigma2, double* out);
+
+/* ======================================================================
  * Host-only plan inspection (no GPU needed): the gossip exchange of one
  * round for one rank, as the engine issues it.  sends: (peer rank, global
  * node id whose bucket is sent); recvs: (peer rank, global node id received),

@@ -98,6 +98,12 @@ class _EngineConfig(C.Structure):
                 ("total_steps", C.c_long), ("transport", C.c_int), ("flags", C.c_int)]
 
 
+class _RmParams(C.Structure):
+    _fields_ = [("N", C.c_int), ("b", C.c_int), ("theta", C.c_double), ("gamma", C.c_double),
+                ("omega", C.c_double), ("sigma2", C.c_double), ("workers_per_node", C.c_int),
+                ("normalized", C.c_int), ("allow_omega_above_one", C.c_int)]
+
+
 class _EngineStats(C.Structure):
     _fields_ = [("local_nodes", C.c_int), ("first_node", C.c_int), ("nodes", C.c_int),
                 ("world_size", C.c_int), ("rank", C.c_int), ("d", C.c_size_t),
@@ -154,6 +160,9 @@ SIGNATURES = {
     "dg_engine_wait_stream": ([_VP, _VP], _I),
     "dg_engine_join": ([_VP, _VP], _I),
     "dg_plan_exchange": ([_VP, _I, _I, _L, _IP, _IP, _IP, _IP, _IP, _IP, _I], _I),
+    "dg_rm_simulate": ([_I, C.POINTER(_RmParams), _VP, _L, C.c_uint64, _DP, _DP], _I),
+    "dg_rm_closed_form_speedup": ([_D, _I, _I, _D, _DP], _I),
+    "dg_rm_speed_multiplier": ([C.c_uint64, C.c_uint64, C.c_uint64, _D, _DP], _I),
 }
 
 
