@@ -360,7 +360,10 @@ void launch_tma(const RoundPlan& p, const Buffers& bf, int algo, bool fold, size
   a.rows_max = rows_max;
   a.t = t;
   a.div_flag = flag;
-  const size_t smem = 256 + size_t(DG_TMA_STAGES) * rows_max * a.tile * sizeof(float);
+  const size_t stage_bytes = size_t(rows_max) * a.tile * sizeof(float);
+  a.stages = int(std::min<size_t>(DG_TMA_STAGES, (227 * 1024 - 256) / stage_bytes));
+  if (a.stages < 2) config_error("tma: component too large for a 2-stage shared-memory ring");
+  const size_t smem = 256 + size_t(a.stages) * stage_bytes;
   const long long units = ((long long)len + a.tile - 1) / a.tile * a.n_comp;
   if (algo == DG_ALGO_DADAM)
     launch_tma_t<0, false>(a, ns_max, smem, units, st);
