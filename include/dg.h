@@ -188,6 +188,8 @@ typedef struct dg_engine_stats {
   double timed_hbm_bytes;   /* algorithmic HBM bytes of those launches */
   int transport;            /* DG_TRANSPORT_NCCL | DG_TRANSPORT_P2P (1-GPU engines report P2P) */
   long barriers;            /* cross-GPU step barriers issued */
+  double remote_kernel_ms;  /* timed fused launches that read remote buckets in-kernel (P2P) */
+  double remote_bytes;      /* NVLink bytes those launches read */
 } dg_engine_stats;
 
 /* ncclGetUniqueId (call on rank 0, broadcast the 128 bytes to all ranks) */
