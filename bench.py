@@ -406,6 +406,16 @@ def run_ours(a):
                               "model": ("SURVEY.md 8(d): per round, max over GPUs of max(HBM bytes/BW_HBM, "
                                         f"NVLink bytes/770 GB/s), {transport} transport"),
                               "nvlink_bytes_received_per_step": st["bytes_received"] / max(1, st["steps"])},
+            "nvlink": ({"achieved": st["remote_bytes"] / (st["remote_kernel_ms"] / 1e3) / 1e9,
+                        "peak": NVL_MEASURED / 1e9, "nominal": 900.0, "unit": "GB/s",
+                        "frac": st["remote_bytes"] / (st["remote_kernel_ms"] / 1e3) / NVL_MEASURED,
+                        "frac_of_nominal": st["remote_bytes"] / (st["remote_kernel_ms"] / 1e3) / 900e9,
+                        "bytes_per_step": st["remote_bytes"] / a.steps,
+                        "kernel_ms_per_step": st["remote_kernel_ms"] / a.steps,
+                        "what": "remote x^(t-1) buckets read in-kernel over NVLink by the exchange-round "
+                                "fused launches (per direction; every GPU both reads and serves)",
+                        "peak_source": "measured peer read bandwidth, B200_PROFILING.md (775 GB/s LDG.128)"}
+                       if st["remote_kernel_ms"] > 0 else None),
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
             "nvlink_bytes_sent_per_step": st["bytes_sent"] / max(1, st["steps"]),
             "nccl_version": st["nccl_version"],

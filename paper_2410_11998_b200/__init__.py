@@ -111,7 +111,7 @@ class _EngineStats(C.Structure):
                 ("bytes_sent", C.c_double), ("bytes_received", C.c_double),
                 ("hbm_bytes", C.c_double), ("nccl_version", C.c_long), ("kernel_ms", C.c_double),
                 ("timed_launches", C.c_long), ("timed_hbm_bytes", C.c_double), ("transport", C.c_int),
-                ("barriers", C.c_long)]
+                ("barriers", C.c_long), ("remote_kernel_ms", C.c_double), ("remote_bytes", C.c_double)]
 
 
 _lib = None

@@ -413,7 +413,9 @@ struct dg_engine {
   void harvest_timing();
   // times (optionally) and counts one launch of ours on the compute stream
   template <class F>
-  void timed(double bytes, F&& launch);
+  void timed(double bytes, double nvl_bytes, F&& launch);
+  std::vector<double> tev_remote;  // NVLink bytes read in-kernel per timed launch
+  double remote_ms = 0, remote_bytes = 0;
   // bucketed steps (f1)
   bool in_place = false;
   float* rbuf = nullptr;                     // [max_recv][d_pad] recv buffers for step_range
@@ -519,31 +521,20 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   const double per = algo == DG_ALGO_DADAM ? 28.0 : (fold ? 36.0 : 28.0);
   const double remote_hbm = transport == DG_TRANSPORT_P2P ? 0.0 : 4.0 * double(p.recv_node.size());
   const double bytes = double(len) * (per * p.n_local + remote_hbm);
-  if (timing) {
-    if (tev_used == tev.size()) {
-      cudaEvent_t a, b;
-      CU(cudaEventCreate(&a));
-      CU(cudaEventCreate(&b));
-      tev.push_back({a, b});
-      tev_bytes.push_back(0);
-    }
-    CU(cudaEventRecord(tev[tev_used].first, comp));
-  }
-  if (tma)
-    dg::launch_tma(p, bf, algo, fold, off, len, s, int(t), flag, comp);
-  else
-    fnh.fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), sms_for(p), comp);
-  dg::cuda_check(cudaGetLastError(), "fused kernel launch");
-  if (timing) {
-    CU(cudaEventRecord(tev[tev_used].second, comp));
-    tev_bytes[tev_used++] = bytes;
-  }
-  ++launches;
-  hbm += bytes;
+  // NVLink bytes the launch reads in-kernel (P2P exchange rounds)
+  const double nvl = (transport == DG_TRANSPORT_P2P && !slot_override)
+                         ? 4.0 * double(len) * double(p.recv_node.size())
+                         : 0.0;
+  timed(bytes, nvl, [&] {
+    if (tma)
+      dg::launch_tma(p, bf, algo, fold, off, len, s, int(t), flag, comp);
+    else
+      fnh.fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), sms_for(p), comp);
+  });
 }
 
 template <class F>
-void dg_engine::timed(double bytes, F&& launch) {
+void dg_engine::timed(double bytes, double nvl_bytes, F&& launch) {
   if (timing) {
     if (tev_used == tev.size()) {
       cudaEvent_t a, b;
@@ -551,6 +542,7 @@ void dg_engine::timed(double bytes, F&& launch) {
       CU(cudaEventCreate(&b));
       tev.push_back({a, b});
       tev_bytes.push_back(0);
+      tev_remote.push_back(0);
     }
     CU(cudaEventRecord(tev[tev_used].first, comp));
   }
@@ -558,6 +550,7 @@ void dg_engine::timed(double bytes, F&& launch) {
   dg::cuda_check(cudaGetLastError(), "kernel launch");
   if (timing) {
     CU(cudaEventRecord(tev[tev_used].second, comp));
+    tev_remote[tev_used] = nvl_bytes;
     tev_bytes[tev_used++] = bytes;
   }
   ++launches;
@@ -575,12 +568,12 @@ void dg_engine::step_allreduce(long t, const dg::DevScalars& s) {
   }
   const unsigned grid = dg::grid_for((long long)d, 8);
   // column sums of the resident gradients: read NL x 4 B, write 8 B per element
-  timed(double(d) * (4.0 * NL + 8.0), [&] {
+  timed(double(d) * (4.0 * NL + 8.0), 0.0, [&] {
     dg::column_sum<<<grid, 256, 0, comp>>>(gsum, g, NL, (long long)d);
   });
   if (G > 1) NC(ncclAllReduce(gsum, gsum, d, ncclDouble, ncclSum, nccl, comp));  // the All-Reduce
   // update: read gsum 8 B + x, m, v; write x, m, v
-  timed(double(d) * (24.0 * NL + 8.0), [&] {
+  timed(double(d) * (24.0 * NL + 8.0), 0.0, [&] {
     dg::allreduce_adam<<<grid, 256, 0, comp>>>(x, m, v, NL, gsum, 1.0 / double(N), (long long)d, s, int(t), flag,
                                                inv_flag);
   });
@@ -593,6 +586,10 @@ void dg_engine::harvest_timing() {
     kernel_ms += ms;
     timed_bytes += tev_bytes[k];
     ++timed_launches;
+    if (tev_remote[k] > 0) {
+      remote_ms += ms;
+      remote_bytes += tev_remote[k];
+    }
   }
   tev_used = 0;
 }
@@ -1054,6 +1051,8 @@ int dg_engine_get_stats(const dg_engine* e, dg_engine_stats* o) {
     o->timed_hbm_bytes = e->timed_bytes;
     o->transport = e->transport;
     o->barriers = e->barriers;
+    o->remote_kernel_ms = e->remote_ms;
+    o->remote_bytes = e->remote_bytes;
   });
 }
 
@@ -1064,7 +1063,7 @@ int dg_engine_set_timing(dg_engine* e, int on) {
     if (!on) {
       CU(cudaStreamSynchronize(e->comp));
       e->tev_used = 0;
-      e->kernel_ms = e->timed_bytes = 0;
+      e->kernel_ms = e->timed_bytes = e->remote_ms = e->remote_bytes = 0;
       e->timed_launches = 0;
     }
     e->timing = on != 0;
