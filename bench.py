@@ -42,7 +42,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--nodes-per-gpu", type=int, default=8)
-    p.add_argument("--d", type=int, default=125_000_000)
+    p.add_argument("--bucket-params", dest="d", type=int, default=125_000_000)
     p.add_argument("--topology", default="one_peer_exponential",
                    choices=["one_peer_exponential", "one_peer_ring", "static_exponential", "aer"])
     p.add_argument("--algo", choices=["dadam", "accum", "allreduce"], default="dadam")

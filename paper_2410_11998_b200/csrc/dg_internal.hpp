@@ -97,6 +97,11 @@ struct RoundPlan {
   // component reading x^(t-1) from the current x buffer and writing x^(t) to
   // the other one (large mixing components; see make_pingpong)
   bool pingpong = false;
+  // P2P transport: pull each distinct remote bucket once into local slots with
+  // the copy engines (set when resident nodes read the same remote buckets
+  // >= 1.75x on average: in-kernel peer loads bypass the local L2 and cross
+  // NVLink once per reader, but run ~1.8x faster than copy-engine pulls)
+  bool pull = false;
   // exchange (ordered by (peer, node))
   std::vector<int> send_peer, send_node;  // send_node: global id of a resident node
   std::vector<int> recv_peer, recv_node;  // recv slot r holds recv_node[r]

@@ -436,6 +436,8 @@ struct dg_engine {
   std::vector<float*> peer_base[2];  // [buffer][rank]; own rank = own pointers
   std::vector<char> round_remote;    // per round: any rank mixes a remote bucket
   float* bar_buf = nullptr;          // 1-element all-reduce = cross-GPU step barrier
+  std::vector<cudaStream_t> pull;    // copy-engine pull streams (pull rounds)
+  std::vector<cudaEvent_t> pull_ev;
   long barriers = 0;
   const float* peer_x(int node) const {
     const int owner = dg::owner_of(node, N, G);
@@ -490,6 +492,8 @@ dg_engine::~dg_engine() {
   }
   if (comp) cudaStreamDestroy(comp);
   if (comm) cudaStreamDestroy(comm);
+  for (auto st : pull) cudaStreamDestroy(st);
+  for (auto ev : pull_ev) cudaEventDestroy(ev);
 }
 
 void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
@@ -519,7 +523,8 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   // algorithmic LOCAL HBM bytes of this launch (remote buckets: recv-slot reads
   // for NCCL; for P2P they come over NVLink and are counted in `received`)
   const double per = algo == DG_ALGO_DADAM ? 28.0 : (fold ? 36.0 : 28.0);
-  const double remote_hbm = transport == DG_TRANSPORT_P2P ? 0.0 : 4.0 * double(p.recv_node.size());
+  const double remote_hbm =
+      (transport == DG_TRANSPORT_P2P && !slot_override) ? 0.0 : 4.0 * double(p.recv_node.size());
   const double bytes = double(len) * (per * p.n_local + remote_hbm);
   // NVLink bytes the launch reads in-kernel (P2P exchange rounds)
   const double nvl = (transport == DG_TRANSPORT_P2P && !slot_override)
@@ -664,9 +669,37 @@ void dg_engine::step(long t) {
       NC(ncclAllReduce(bar_buf, bar_buf, 1, ncclFloat, ncclSum, nccl, comp));
       ++barriers;
     }
-    enqueue_fused(p, 0, d, 0, s, fold, t);  // remote sources read over NVLink inside the kernel
     sent += 4.0 * double(d) * double(p.send_node.size());
     received += 4.0 * double(d) * double(p.recv_node.size());
+    if (!p.pull) {
+      enqueue_fused(p, 0, d, 0, s, fold, t);  // remote sources read over NVLink inside the kernel
+    } else {
+      // copy-engine pulls of each distinct remote bucket, chunk by chunk into
+      // double-buffered local slots, overlapped with the kernel on the previous chunk
+      CU(cudaEventRecord(ev_begin, comp));  // after the barrier: peers' x^(t-1) final
+      const int np = std::min<int>(int(pull.size()), int(p.recv_node.size()));
+      for (int q = 0; q < np; ++q) CU(cudaStreamWaitEvent(pull[q], ev_begin, 0));
+      const float* slot_ptr[dg::kMaxRemote];
+      for (size_t k = 0; k < n_chunks; ++k) {
+        const size_t off = k * chunk, len = std::min(chunk, d - off);
+        const int set = int(k & 1);
+        for (int q = 0; q < np; ++q)
+          if (k >= 2) CU(cudaStreamWaitEvent(pull[q], ev_slot_free[set], 0));
+        // one copy stream per remote bucket (round robin): concurrent copy engines
+        for (size_t r = 0; r < p.recv_node.size(); ++r) {
+          float* dst = slots + (size_t(set) * max_recv + r) * chunk;
+          CU(cudaMemcpyAsync(dst, peer_x(p.recv_node[r]) + off, len * sizeof(float), cudaMemcpyDeviceToDevice,
+                             pull[r % np]));
+          slot_ptr[r] = dst;
+        }
+        for (int q = 0; q < np; ++q) {
+          CU(cudaEventRecord(pull_ev[q], pull[q]));
+          CU(cudaStreamWaitEvent(comp, pull_ev[q], 0));
+        }
+        enqueue_fused(p, off, len, set, s, fold, t, slot_ptr);
+        CU(cudaEventRecord(ev_slot_free[set], comp));
+      }
+    }
     if (p.pingpong) xcur ^= 1;
     return;
   }
@@ -778,6 +811,19 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
         dg::make_pingpong(e->plans[r], e->first);
         any_pp = true;
       }
+      // P2P pull decision: some remote bucket is read by more than one resident row
+      auto& pr = e->plans[r];
+      long remote_reads = 0;
+      for (const auto& cp : pr.comps)
+        for (const auto& row : cp.w)
+          for (size_t k = 0; k < cp.srcs.size(); ++k)
+            if (cp.srcs[k] < 0 && row[k] != 0.0) ++remote_reads;
+      const char* pv = std::getenv("DG_P2P_PULL");  // 0 never, 1 auto (default), 2 always
+      const int pull_mode = pv ? std::atoi(pv) : 1;
+      // in-kernel peer loads reach ~770 GB/s, copy-engine pulls ~420 GB/s (measured):
+      // pull only when a remote bucket is read >= 1.75x on average
+      pr.pull = p2p && !pr.recv_node.empty() &&
+                (pull_mode == 2 || (pull_mode == 1 && 4 * remote_reads >= 7 * long(pr.recv_node.size())));
     }
     if (e->NL < 1) dg::config_error("engine_create: no resident nodes on this rank");
     CU(cudaSetDevice(c->device));
@@ -802,7 +848,20 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       CU(cudaMalloc(&e->x_alt, sizeof(float) * e->d_pad * e->NL));
       CU(cudaMemsetAsync(e->x_alt, 0, sizeof(float) * e->d_pad * e->NL, e->comp));
     }
-    if (e->max_recv && !p2p) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
+    bool any_pull = false;
+    for (const auto& pr : e->plans) any_pull |= pr.pull;
+    if (any_pull) {
+      const char* ps = std::getenv("DG_PULL_STREAMS");  // measured: 1 and 8 streams perform alike
+      const int nps = std::max(1, std::min(e->max_recv, ps ? std::atoi(ps) : 2));
+      e->pull.resize(nps);
+      e->pull_ev.resize(nps);
+      for (int q = 0; q < nps; ++q) {
+        CU(cudaStreamCreateWithPriority(&e->pull[q], cudaStreamNonBlocking, hi));
+        CU(cudaEventCreateWithFlags(&e->pull_ev[q], cudaEventDisableTiming));
+      }
+    }
+    if (e->max_recv && (!p2p || any_pull))
+      CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
     CU(cudaMalloc(&e->flag, sizeof(int)));
     CU(cudaMalloc(&e->inv_flag, sizeof(int)));
     const int none = INT_MAX;
@@ -856,7 +915,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
           }
       e->transport = DG_TRANSPORT_NCCL;
       p2p = false;
-      if (e->max_recv) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
+      if (e->max_recv && !e->slots) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
     }
     *out = e.release();
   });
@@ -1002,6 +1061,7 @@ int dg_engine_sync(dg_engine* e) {
     if (!e) dg::config_error("engine_sync: null handle");
     CU(cudaSetDevice(e->device));
     CU(cudaStreamSynchronize(e->comm));
+    for (auto st : e->pull) CU(cudaStreamSynchronize(st));
     CU(cudaStreamSynchronize(e->comp));
     if (e->nccl) {
       ncclResult_t ar;

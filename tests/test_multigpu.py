@@ -26,13 +26,14 @@ def _port():
 
 @pytest.mark.parametrize("world", sorted({2, min(4, torch.cuda.device_count())}))
 @pytest.mark.parametrize("d,chunk", [(100_003, 16384), (1 << 20, 0)])
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "nccl", "p2p_pull_always", "p2p_direct_only"])
 def test_multigpu_bit_exact(world, d, chunk, transport):
     if world > torch.cuda.device_count():
         pytest.skip("not enough GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_parity_main.py")]
-    env = {**os.environ, "MP_D": str(d), "MP_CHUNK": str(chunk), "MP_TRANSPORT": transport}
+    extra = {"p2p_pull_always": {"DG_P2P_PULL": "2"}, "p2p_direct_only": {"DG_P2P_PULL": "0"}}.get(transport, {})
+    env = {**os.environ, "MP_D": str(d), "MP_CHUNK": str(chunk), "MP_TRANSPORT": transport.split("_")[0], **extra}
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
 
