@@ -808,7 +808,15 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       }
       if (p2p && e->round_remote[r]) pp = true;
       if (pp) {
-        dg::make_pingpong(e->plans[r], e->first);
+        // small components in P2P exchange rounds keep their structure (each
+        // remote source is loaded once per column, in registers) and only
+        // redirect x^(t) to the other buffer; otherwise one gather per node
+        const bool keep = p2p && e->round_remote[r] && e->plans[r].comp_size <= 2 &&
+                          !(std::getenv("DG_P2P_SPLIT") && std::atoi(std::getenv("DG_P2P_SPLIT")));
+        if (keep)
+          e->plans[r].pingpong = true;
+        else
+          dg::make_pingpong(e->plans[r], e->first);
         any_pp = true;
       }
       // P2P pull decision: some remote bucket is read by more than one resident row
