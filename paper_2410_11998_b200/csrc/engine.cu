@@ -307,7 +307,7 @@ void launch_tma_t(const TmaArgs& a, int ns_max, size_t smem, long long units, cu
 
 void launch_tma(const RoundPlan& p, const Buffers& bf, int algo, bool fold, size_t off, size_t len,
                 const DevScalars& s, int t, int* flag, cudaStream_t st) {
-  static TmaArgs a;  // large POD; one engine call at a time per thread of use
+  thread_local TmaArgs a;  // large POD (~9 KB), reused per host thread
   std::memset(&a, 0, sizeof(a));
   const int K = algo == DG_ALGO_ACCUM ? 4 : 3;
   a.n_comp = int(p.comps.size());
@@ -377,10 +377,6 @@ void launch_tma(const RoundPlan& p, const Buffers& bf, int algo, bool fold, size
 }  // namespace dg
 
 // ===================================================================== engine
-struct LaunchFnHolder {
-  dg::LaunchFn fn;
-};
-
 struct dg_engine {
   // configuration
   int N = 0, G = 1, rank = 0, device = 0, algo = 0, first = 0, NL = 0, P = 0;
@@ -401,7 +397,6 @@ struct dg_engine {
   // stats
   long launches = 0, steps = 0;
   double sent = 0, received = 0, hbm = 0;
-  int blocks_per_sm = 4;
   std::vector<unsigned char> argbuf;
   // optional per-launch CUDA-event timing (bench roofline)
   bool timing = false;
@@ -515,10 +510,10 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
                                                   : slots + (size_t(slot_set) * max_recv + r) * chunk;
   const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr};
   const bool tma = dg::use_tma(p);
-  LaunchFnHolder fnh{nullptr};
+  dg::LaunchFn fn = nullptr;
   if (!tma) {
     dg::fill_args(argbuf, p, bf, off, len, s, int(t), flag);
-    fnh.fn = dg::pick(p.comp_size, p.src_bound, algo, fold);
+    fn = dg::pick(p.comp_size, p.src_bound, algo, fold);
   }
   // algorithmic LOCAL HBM bytes of this launch (remote buckets: recv-slot reads
   // for NCCL; for P2P they come over NVLink and are counted in `received`)
@@ -534,7 +529,7 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
     if (tma)
       dg::launch_tma(p, bf, algo, fold, off, len, s, int(t), flag, comp);
     else
-      fnh.fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), sms_for(p), comp);
+      fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), sms_for(p), comp);
   });
 }
 

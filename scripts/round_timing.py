@@ -15,7 +15,7 @@ import paper_2410_11998_b200 as dg  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--nodes-per-gpu", type=int, default=8)
-ap.add_argument("--d", type=int, default=125_000_000)
+ap.add_argument("--bucket-params", dest="d", type=int, default=125_000_000)
 ap.add_argument("--topology", default="one_peer_exponential")
 ap.add_argument("--chunk", type=int, default=0)
 ap.add_argument("--periods", type=int, default=2)
