@@ -815,13 +815,14 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
           dg::make_pingpong(e->plans[r], e->first);
         any_pp = true;
       }
-      // P2P pull decision: some remote bucket is read by more than one resident row
+      // P2P pull decision: NVLink reads per column = remote sources summed over the
+      // components (a component's thread loads each of its sources once; repeats
+      // across member rows hit L1), vs the distinct remote buckets
       auto& pr = e->plans[r];
       long remote_reads = 0;
       for (const auto& cp : pr.comps)
-        for (const auto& row : cp.w)
-          for (size_t k = 0; k < cp.srcs.size(); ++k)
-            if (cp.srcs[k] < 0 && row[k] != 0.0) ++remote_reads;
+        for (size_t k = 0; k < cp.srcs.size(); ++k)
+          if (cp.srcs[k] < 0) ++remote_reads;
       const char* pv = std::getenv("DG_P2P_PULL");  // 0 never, 1 auto (default), 2 always
       const int pull_mode = pv ? std::atoi(pv) : 1;
       // in-kernel peer loads reach ~770 GB/s, copy-engine pulls ~420 GB/s (measured):
