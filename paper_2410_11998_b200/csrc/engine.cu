@@ -806,8 +806,8 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
         // small components in P2P exchange rounds keep their structure (each
         // remote source is loaded once per column, in registers) and only
         // redirect x^(t) to the other buffer; otherwise one gather per node
-        const char* kenv = std::getenv("DG_P2P_KEEP_NC");  // largest component kept whole (default 2)
-        const int keep_nc = kenv ? std::atoi(kenv) : 2;
+        const char* kenv = std::getenv("DG_P2P_KEEP_NC");  // largest component kept whole (default 4)
+        const int keep_nc = kenv ? std::atoi(kenv) : 4;
         const bool keep = p2p && e->round_remote[r] && e->plans[r].comp_size <= keep_nc;
         if (keep)
           e->plans[r].pingpong = true;
