@@ -192,6 +192,7 @@ LaunchFn pick_ns(int ns, int algo, bool fold) {
   // instantiated only for NS >= NC
   if (ns <= 2 && NC <= 2) return pick_algo<NC, (NC <= 2 ? 2 : NC)>(algo, fold);
   if (ns <= 4 && NC <= 4) return pick_algo<NC, (NC <= 4 ? 4 : NC)>(algo, fold);
+  if (ns <= 6 && NC == 1) return pick_algo<1, 6>(algo, fold);  // static-exponential nodes (84 -> 80 regs)
   if (ns <= 8 && NC <= 8) return pick_algo<NC, (NC <= 8 ? 8 : NC)>(algo, fold);
   if (ns <= 16) return pick_algo<NC, 16>(algo, fold);
   return pick_algo<NC, 32>(algo, fold);
