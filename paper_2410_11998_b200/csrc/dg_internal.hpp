@@ -64,7 +64,7 @@ dg_validation validate_dense(const std::vector<double>& w, int n);
 // ------------------------------------------------------------------ plans
 constexpr int kMaxLocal = 16;   // resident nodes per GPU
 constexpr int kMaxDeg = 16;     // neighbours per node (self included)
-constexpr int kMaxRemote = 32;  // distinct remote buckets per round per GPU
+constexpr int kMaxRemote = kMaxLocal * kMaxDeg;  // distinct remote buckets per round per GPU (implied bound)
 
 // Placement: node i lives on rank floor(i*G/N) (SURVEY.md 8 common notation).
 inline int owner_of(int node, int nodes, int world) {
@@ -97,6 +97,8 @@ struct RoundPlan {
   // component reading x^(t-1) from the current x buffer and writing x^(t) to
   // the other one (large mixing components; see make_pingpong)
   bool pingpong = false;
+  // some component has > 32 distinct sources: the round must run ping-pong
+  bool oversize = false;
   // P2P transport: pull each distinct remote bucket once into local slots with
   // the copy engines (set when resident nodes read the same remote buckets
   // >= 1.75x on average: in-kernel peer loads bypass the local L2 and cross

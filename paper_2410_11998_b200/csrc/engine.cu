@@ -799,7 +799,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       bool pp = false;
       for (int g = 0; g < e->G; ++g) {
         const auto q = g == e->rank ? e->plans[r] : dg::build_round_plan(*c->schedule, e->G, g, r + 1);
-        if (pp_min > 0 && q.comp_size >= pp_min) pp = true;
+        if ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize) pp = true;
         if (!q.recv_node.empty()) e->round_remote[r] = 1;
       }
       if (p2p && e->round_remote[r]) pp = true;
@@ -809,7 +809,8 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
         // redirect x^(t) to the other buffer; otherwise one gather per node
         const char* kenv = std::getenv("DG_P2P_KEEP_NC");  // largest component kept whole (default 4)
         const int keep_nc = kenv ? std::atoi(kenv) : 4;
-        const bool keep = p2p && e->round_remote[r] && e->plans[r].comp_size <= keep_nc;
+        if (e->in_place) dg::config_error("engine: a mixing component has > 32 sources; in-place mode cannot double-buffer x");
+        const bool keep = p2p && e->round_remote[r] && e->plans[r].comp_size <= keep_nc && !e->plans[r].oversize;
         if (keep)
           e->plans[r].pingpong = true;
         else

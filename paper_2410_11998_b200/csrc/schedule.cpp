@@ -212,7 +212,7 @@ dg::RoundPlan dg::build_round_plan(const dg_schedule& s, int world, int rank, lo
       if (j < first || j >= last) need.push_back({owner_of(j, N, world), j});
   std::sort(need.begin(), need.end());
   need.erase(std::unique(need.begin(), need.end()), need.end());
-  if (int(need.size()) > kMaxRemote) config_error("plan: more than 32 remote buckets per round");
+  if (int(need.size()) > kMaxRemote) config_error("plan: too many remote buckets per round");
   for (auto [peer, j] : need) {
     p.recv_peer.push_back(peer);
     p.recv_node.push_back(j);
@@ -296,7 +296,9 @@ dg::RoundPlan dg::build_round_plan(const dg_schedule& s, int world, int rank, lo
       p.comps.push_back(std::move(c));
     }
     p.src_bound = std::max(nsb, cs);
-    if (p.src_bound > 32) config_error("plan: more than 32 distinct sources in one mixing component");
+    // > 32 distinct sources (e.g. static exponential over many GPUs): the round
+    // can only run x double-buffered, one gather per node (make_pingpong)
+    p.oversize = p.src_bound > 32;
   }
   // sends: resident node j goes to every other rank hosting a node that mixes j
   std::vector<std::pair<int, int>> sends;

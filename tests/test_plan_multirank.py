@@ -1,4 +1,4 @@
-"""Multi-GPU host logic on CPU: world_size 2 / 4 gloo ranks each build their
+"""Multi-GPU host logic on CPU: world_size 2 / 4 / 8 gloo ranks each build their
 round plans through libdg (dg_plan_exchange) and check, via gloo collectives,
 that every rank's sends to a peer are exactly that peer's receives from it, in
 the same (node-ascending) order NCCL's per-peer in-order matching needs, and
@@ -12,7 +12,8 @@ import torch.multiprocessing as mp
 
 CASES = [("make_one_peer_exponential", (8,)), ("make_one_peer_exponential", (64,)),
          ("make_one_peer_ring", (8,)), ("make_static_exponential", (8,)), ("make_aer", (8, 2)),
-         ("make_aer", (16, 2)), ("make_complete", (8,))]
+         ("make_aer", (16, 2)), ("make_complete", (8,)), ("make_static_exponential", (64,)),
+         ("make_aer", (64, 8))]
 
 
 def _free_port():
@@ -64,7 +65,7 @@ def _worker(rank, world, port, q):
         q.put((rank, repr(e)))
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_plans_match_across_ranks(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
