@@ -228,6 +228,17 @@ def cpu_reference_run(a, nodes_sample, d_sample, steps, threads):
     return nodes_sample * d_sample * steps / el, kind, note, el
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(a, budget_s):
     import numpy as np  # noqa: F401
     threads = os.cpu_count() or 1
@@ -236,7 +247,10 @@ def cpu_baseline(a, budget_s):
     rate, _, _, el = cpu_reference_run(a, nodes_sample, d_sample, 2, threads)
     steps = max(3, int(budget_s * rate / (nodes_sample * d_sample)))
     rate, kind, note, el = cpu_reference_run(a, nodes_sample, d_sample, steps, threads)
+    # Exec::Serial: one thread, a quarter of the sample
+    serial, _, _, _ = cpu_reference_run(a, nodes_sample, d_sample, max(2, steps // 4), 1)
     return {"value": rate, "unit": UNIT, "cores": min(threads, nodes_sample), "host_threads": threads,
+            "serial_value": serial, "cpu_model": cpu_model(),
             "kind": kind,
             "sample": (f"{nodes_sample} nodes x {d_sample:,} params (fp64), {steps} steps of the same "
                        f"topology/algorithm, g held fixed; {el:.1f} s wall; OpenMP over nodes "
@@ -259,6 +273,7 @@ def run_reference(a):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_block(a, world, nodes),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": min(threads, nodes_sample), "kind": kind,
+                         "cpu_model": cpu_model(),
                          "sample": f"{nodes_sample} nodes x {d_sample:,} params per step (bounded sample of "
                                    f"the workload), {a.warmup + a.steps} steps, {el:.1f} s; {note}"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
