@@ -163,10 +163,35 @@ void launch_coop(const void* args, long long cols, int n_comp, int sms, cudaStre
   kern<<<grid, threads, 0, st>>>(*static_cast<const FusedArgs<NC, NS>*>(args));
 }
 
+int warps_min_nc() {  // DG_WARPS_MIN_NC: fewest single-member components run one warp per node
+  static const int v = [] {
+    const char* e = std::getenv("DG_WARPS_MIN_NC");
+    return e ? std::atoi(e) : 99;
+  }();
+  return v;
+}
+template <int NS, int ALGO, bool FOLD>
+void launch_warps(const void* args, long long cols, int n_comp, int sms, cudaStream_t st) {
+  auto kern = gossip_adam_warps<NS, ALGO, FOLD>;
+  const int threads = 32 * n_comp;
+  static int occ_by_nc[9] = {};
+  int& occ = occ_by_nc[n_comp];
+  if (!occ) {
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, 0), "occupancy");
+    occ = std::max(1, occ);
+  }
+  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * sms));
+  const long long need = (cols + 31) / 32;
+  kern<<<unsigned(std::max(1LL, std::min(resident, need))), threads, 0, st>>>(
+      *static_cast<const FusedArgs<1, NS>*>(args));
+}
+
 template <int NC, int NS, int ALGO, bool FOLD>
 void launch_fused(const void* args, long long cols, int n_comp, int sms, cudaStream_t st) {
   if constexpr (NC >= 2) {
     if (NC >= coop_min_nc()) return launch_coop<NC, NS, ALGO, FOLD>(args, cols, n_comp, sms, st);
+  } else {
+    if (n_comp >= warps_min_nc() && n_comp <= 8) return launch_warps<NS, ALGO, FOLD>(args, cols, n_comp, sms, st);
   }
   auto kern = gossip_adam_fused<NC, NS, ALGO, FOLD>;
   constexpr int threads = LaunchShape<NC, NS>::threads;
@@ -248,12 +273,21 @@ void fill_args_t(std::vector<unsigned char>& buf, const RoundPlan& p, const Buff
   a->t = t;
   a->div_flag = flag;
 }
+// source count that selects the NS instantiation: the largest actual source
+// count of the plan's components (src_bound is rounded up to a power of two).
+// pick() and fill_args() must agree on it (same FusedArgs<NC, NS> layout).
+int launch_ns(const RoundPlan& p) {
+  size_t ns = 1;
+  for (const auto& c : p.comps) ns = std::max(ns, c.srcs.size());
+  return int(ns);
+}
 template <int NC>
 void fill_ns(std::vector<unsigned char>& buf, const RoundPlan& p, const Buffers& bf, size_t off,
              size_t len, const DevScalars& s, int t, int* flag) {
-  const int ns = p.src_bound;
+  const int ns = launch_ns(p);
   if (ns <= 2 && NC <= 2) return fill_args_t<NC, (NC <= 2 ? 2 : NC)>(buf, p, bf, off, len, s, t, flag);
   if (ns <= 4 && NC <= 4) return fill_args_t<NC, (NC <= 4 ? 4 : NC)>(buf, p, bf, off, len, s, t, flag);
+  if (ns <= 6 && NC == 1) return fill_args_t<1, 6>(buf, p, bf, off, len, s, t, flag);
   if (ns <= 8 && NC <= 8) return fill_args_t<NC, (NC <= 8 ? 8 : NC)>(buf, p, bf, off, len, s, t, flag);
   if (ns <= 16) return fill_args_t<NC, 16>(buf, p, bf, off, len, s, t, flag);
   return fill_args_t<NC, 32>(buf, p, bf, off, len, s, t, flag);
@@ -514,7 +548,7 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   dg::LaunchFn fn = nullptr;
   if (!tma) {
     dg::fill_args(argbuf, p, bf, off, len, s, int(t), flag);
-    fn = dg::pick(p.comp_size, p.src_bound, algo, fold);
+    fn = dg::pick(p.comp_size, dg::launch_ns(p), algo, fold);
   }
   // algorithmic LOCAL HBM bytes of this launch (remote buckets: recv-slot reads
   // for NCCL; for P2P they come over NVLink and are counted in `received`)

@@ -18,7 +18,8 @@ PATHS = {"default": {},
          "tma_all": {"DG_TMA": "2", "DG_PINGPONG_MIN_NC": "0"},
          "tma_pingpong": {"DG_TMA": "2", "DG_PINGPONG_MIN_NC": "1"},
          "per_thread_all": {"DG_TMA": "0", "DG_COOP_MIN_NC": "99", "DG_PINGPONG_MIN_NC": "0"},
-         "coop_all": {"DG_TMA": "0", "DG_COOP_MIN_NC": "2", "DG_PINGPONG_MIN_NC": "0"}}
+         "coop_all": {"DG_TMA": "0", "DG_COOP_MIN_NC": "2", "DG_PINGPONG_MIN_NC": "0"},
+         "warps_all": {"DG_TMA": "0", "DG_PINGPONG_MIN_NC": "1", "DG_WARPS_MIN_NC": "1"}}
 
 
 @pytest.mark.parametrize("path", sorted(PATHS))
