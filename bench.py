@@ -415,7 +415,8 @@ def run_ours(a):
                          "bytes_per_param_update": HBM_PER_UPDATE,
                          "kernel_ms_per_launch": st["kernel_ms"] / max(1, st["timed_launches"]),
                          "kernel_share_of_step": st["kernel_ms"] / ms if ms > 0 else None,
-                         "peak_source": peak_src, "kernel": "gossip_adam_fused"},
+                         "peak_source": peak_src,
+                         "kernel": "gossip_adam_fused (gossip_adam_warps for rounds of 4-8 single-node components)"},
             "step_roofline": {"bound_ms_per_step": 1e3 * roof_step_s / a.steps,
                               "frac": (roof_step_s * 1e3) / ms_max,
                               "model": ("SURVEY.md 8(d): per round, max over GPUs of max(HBM bytes/BW_HBM, "
