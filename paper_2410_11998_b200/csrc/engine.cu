@@ -841,11 +841,13 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       }
       if (p2p && e->round_remote[r]) pp = true;
       if (pp) {
-        // small components in P2P exchange rounds keep their structure (each
+        // pair components in P2P exchange rounds keep their structure (each
         // remote source is loaded once per column, in registers) and only
         // redirect x^(t) to the other buffer; otherwise one gather per node
-        const char* kenv = std::getenv("DG_P2P_KEEP_NC");  // largest component kept whole (default 4)
-        const int keep_nc = kenv ? std::atoi(kenv) : 4;
+        // (4-8 nodes: one warp per node in a CTA, so remote lines are shared
+        // through L1 -- config 3 at 2 GPUs: 9.2 ms vs 10.8 ms kept whole)
+        const char* kenv = std::getenv("DG_P2P_KEEP_NC");  // largest component kept whole (default 2)
+        const int keep_nc = kenv ? std::atoi(kenv) : 2;
         if (e->in_place) dg::config_error("engine: a mixing component has > 32 sources; in-place mode cannot double-buffer x");
         const bool keep = p2p && e->round_remote[r] && e->plans[r].comp_size <= keep_nc && !e->plans[r].oversize;
         if (keep)
@@ -856,12 +858,15 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       }
       // P2P pull decision: NVLink reads per column = remote sources summed over the
       // components (a component's thread loads each of its sources once; repeats
-      // across member rows hit L1), vs the distinct remote buckets
+      // across member rows hit L1), vs the distinct remote buckets.  With one warp
+      // per node (gossip_adam_warps) the CTA shares every remote line: distinct.
       auto& pr = e->plans[r];
       long remote_reads = 0;
       for (const auto& cp : pr.comps)
         for (size_t k = 0; k < cp.srcs.size(); ++k)
           if (cp.srcs[k] < 0) ++remote_reads;
+      const int ncomp = int(pr.comps.size());
+      if (pr.comp_size == 1 && ncomp >= dg::warps_min_nc() && ncomp <= 8) remote_reads = long(pr.recv_node.size());
       const char* pv = std::getenv("DG_P2P_PULL");  // 0 never, 1 auto (default), 2 always
       const int pull_mode = pv ? std::atoi(pv) : 1;
       // in-kernel peer loads reach ~770 GB/s, copy-engine pulls ~420 GB/s (measured):
