@@ -59,3 +59,15 @@ def test_errors_map_to_reference_taxonomy(dg):
         dg.make_aer(6, 4)
     assert e.value.code == 2 and isinstance(e.value, ValueError)
     assert dg.DivergenceError.code == 3 and dg.InvariantError.code == 4
+
+
+def test_every_engine_knob_is_documented():
+    """Every environment knob the library reads is listed in INTEGRATION.md section 7."""
+    import glob
+    root = ROOT
+    knobs = set()
+    for f in glob.glob(os.path.join(root, "paper_2410_11998_b200", "csrc", "*.*")):
+        if f.endswith((".cu", ".cuh", ".cpp", ".hpp")):
+            knobs |= set(re.findall(r'getenv\("([A-Z_0-9]+)"\)', open(f).read()))
+    doc = open(os.path.join(root, "INTEGRATION.md")).read()
+    assert knobs and all(f"`{k}`" in doc for k in knobs), sorted(k for k in knobs if f"`{k}`" not in doc)
