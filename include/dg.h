@@ -62,6 +62,14 @@ int dg_make_static_exponential(int n, dg_schedule** out);
  * w: period x n x n row-major; validates every round + union connectivity */
 int dg_schedule_from_matrices(const double* w, int n, int period, int workers_per_node,
                               dg_schedule** out);
+/* from_matrices with the schedule's name (topology.hpp:44-45; the unnamed form
+ * above names it "custom") */
+int dg_schedule_from_matrices_named(const char* name, const double* w, int n, int period,
+                                    int workers_per_node, dg_schedule** out);
+/* name()  topology.hpp:50 -- "complete", "one_peer_ring", "one_peer_exponential",
+ * "aer", "static_exponential" for the builders.  Copies a NUL-terminated string
+ * into buf (cap bytes; DG_CONFIG_ERROR if too small); *len = strlen(name). */
+int dg_schedule_name(const dg_schedule* s, char* buf, size_t cap, size_t* len);
 /* workers() / period() / workers_per_node() / is_static()   topology.hpp:47-51 */
 int dg_schedule_info(const dg_schedule* s, int* workers, int* period, int* workers_per_node,
                      int* is_static);
@@ -79,6 +87,11 @@ typedef struct dg_validation {
   int symmetric, nonnegative, rows_stochastic, cols_stochastic, eigenvalues_in_range;
   double max_asymmetry, min_entry, max_row_error, max_col_error, min_eigenvalue, max_eigenvalue;
 } dg_validation;
+/* MixingValidation::pass() (topology.hpp:29-32): 1 if every check passed */
+int dg_validation_pass(const dg_validation* v);
+/* MixingValidation::describe() (topology.hpp:33): one-line human-readable
+ * report; same buffer contract as dg_schedule_name */
+int dg_validation_describe(const dg_validation* v, char* buf, size_t cap, size_t* len);
 /* validate(W)                 topology.hpp:80 */
 int dg_validate(const double* w, int n, dg_validation* out);
 /* spectral_lambda(W)          topology.hpp:82-84 (DG_CONFIG_ERROR if not symmetric) */
@@ -222,6 +235,10 @@ int dg_engine_fill_synthetic(dg_engine* e, int which, uint64_t seed, uint32_t pu
  * *mean_sq = ||xbar||^2.  gossip_consensus's error[t] (topology.hpp:90-96) is
  * dispersion_t / dispersion_0. */
 int dg_engine_consensus(dg_engine* e, double* dispersion, double* mean_sq);
+/* Fixes xbar for every later dg_engine_consensus call to the CURRENT column
+ * mean (collective, synchronous): gossip_consensus measures dispersion around
+ * the preserved initial mean xbar^(0) (topology.hpp:90-94). */
+int dg_engine_consensus_fix_mean(dg_engine* e);
 /* One fused gossip + Adam step for iteration t (>= 1); asynchronous. */
 int dg_engine_step(dg_engine* e, long t);
 /* Bucketed step (the paper's per-bucket update U_k, PAPER.md:302-304 and
@@ -250,6 +267,9 @@ int dg_engine_get_stats(const dg_engine* e, dg_engine_stats* out);
  * durations are harvested into kernel_ms at dg_engine_sync.  on == 0 stops
  * and also resets kernel_ms / timed_launches / timed_hbm_bytes. */
 int dg_engine_set_timing(dg_engine* e, int on);
+/* Frees the engine.  COLLECTIVE for multi-GPU engines on the P2P transport:
+ * every rank calls it (a final stream-ordered barrier keeps this rank's
+ * exported x buffers mapped until every peer's last kernel has read them). */
 void dg_engine_destroy(dg_engine* e);
 
 /* ======================================================================

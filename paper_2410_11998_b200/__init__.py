@@ -27,6 +27,7 @@ __all__ = [
     "validate", "spectral_lambda", "effective_lambda", "OptimizerConfig", "gossip_mix",
     "dadam_step", "accum_adam_step", "check_divergence", "fill_synthetic", "Engine",
     "nccl_unique_id", "plan_exchange", "library_path", "DADAM", "ACCUM", "ALLREDUCE", "gossip_consensus",
+    "ConsensusTrajectory",
     "TRANSPORT_AUTO", "TRANSPORT_NCCL", "TRANSPORT_P2P",
     "X", "G", "M", "V", "ACC", "Stream",
 ]
@@ -130,6 +131,10 @@ SIGNATURES = {
     "dg_make_aer": ([_I, _I, C.POINTER(_VP)], _I),
     "dg_make_static_exponential": ([_I, C.POINTER(_VP)], _I),
     "dg_schedule_from_matrices": ([_DP, _I, _I, _I, C.POINTER(_VP)], _I),
+    "dg_schedule_from_matrices_named": ([C.c_char_p, _DP, _I, _I, _I, C.POINTER(_VP)], _I),
+    "dg_schedule_name": ([_VP, C.c_char_p, _SZ, C.POINTER(_SZ)], _I),
+    "dg_validation_pass": ([C.POINTER(_Validation)], _I),
+    "dg_validation_describe": ([C.POINTER(_Validation), C.c_char_p, _SZ, C.POINTER(_SZ)], _I),
     "dg_schedule_info": ([_VP, _IP, _IP, _IP, _IP], _I),
     "dg_schedule_neighbors": ([_VP, _L, _I, _IP, _DP, _I, _IP], _I),
     "dg_schedule_matrix": ([_VP, _L, _DP], _I),
@@ -150,6 +155,7 @@ SIGNATURES = {
     "dg_engine_fill_synthetic": ([_VP, _I, C.c_uint64, C.c_uint32, _I, C.c_uint64], _I),
     "dg_engine_gather": ([_VP, _I, _I, _VP, _SZ, _VP], _I),
     "dg_engine_consensus": ([_VP, _DP, _DP], _I),
+    "dg_engine_consensus_fix_mean": ([_VP], _I),
     "dg_engine_step": ([_VP, _L], _I),
     "dg_engine_sync": ([_VP], _I),
     "dg_engine_streams": ([_VP, C.POINTER(_VP), C.POINTER(_VP)], _I),
@@ -215,17 +221,32 @@ class MixingValidation:
     min_eigenvalue: float
     max_eigenvalue: float
 
-    def passed(self) -> bool:  # MixingValidation::pass()
-        return (self.symmetric and self.nonnegative and self.rows_stochastic
-                and self.cols_stochastic and self.eigenvalues_in_range)
+    def _c(self):
+        return _Validation(*(int(getattr(self, f)) if i < 5 else float(getattr(self, f))
+                             for i, (f, _) in enumerate(_Validation._fields_)))
+
+    def passed(self) -> bool:  # MixingValidation::pass() (topology.hpp:29-32)
+        c = self._c()
+        return bool(lib().dg_validation_pass(C.byref(c)))
+
+    def describe(self) -> str:  # MixingValidation::describe() (topology.hpp:33)
+        c = self._c()
+        buf = C.create_string_buffer(512)
+        n = C.c_size_t()
+        _check(lib().dg_validation_describe(C.byref(c), buf, len(buf), C.byref(n)))
+        return buf.value.decode()
 
 
 class MixingSchedule:
     """Immutable periodic mixing schedule (topology.hpp:40-63); 1-based rounds."""
 
-    def __init__(self, handle: int, name: str):
+    def __init__(self, handle: int):
         self._h = C.c_void_p(handle)
-        self._name = name
+        n = C.c_size_t()
+        _check(lib().dg_schedule_name(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib().dg_schedule_name(self._h, buf, len(buf), C.byref(n)))
+        self._name = buf.value.decode()
         w, p, k, s = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         _check(lib().dg_schedule_info(self._h, C.byref(w), C.byref(p), C.byref(k), C.byref(s)))
         self._workers, self._period, self._wpn, self._static = w.value, p.value, k.value, bool(s.value)
@@ -249,7 +270,7 @@ class MixingSchedule:
     def workers_per_node(self) -> int:
         return self._wpn
 
-    def name(self) -> str:
+    def name(self) -> str:  # topology.hpp:50 (dg_schedule_name)
         return self._name
 
     def is_static(self) -> bool:
@@ -276,30 +297,30 @@ class MixingSchedule:
         return out
 
 
-def _make(fn, name, *args):
+def _make(fn, *args):
     h = C.c_void_p()
     _check(fn(*args, C.byref(h)))
-    return MixingSchedule(h.value, name)
+    return MixingSchedule(h.value)
 
 
 def make_complete(n: int) -> MixingSchedule:                      # topology.hpp:65-66
-    return _make(lib().dg_make_complete, "complete", n)
+    return _make(lib().dg_make_complete, n)
 
 
 def make_one_peer_ring(n: int) -> MixingSchedule:                 # topology.hpp:67-69
-    return _make(lib().dg_make_one_peer_ring, "one_peer_ring", n)
+    return _make(lib().dg_make_one_peer_ring, n)
 
 
 def make_one_peer_exponential(n: int) -> MixingSchedule:          # topology.hpp:70-72
-    return _make(lib().dg_make_one_peer_exponential, "one_peer_exponential", n)
+    return _make(lib().dg_make_one_peer_exponential, n)
 
 
 def make_aer(n: int, workers_per_node: int) -> MixingSchedule:    # topology.hpp:73-78
-    return _make(lib().dg_make_aer, "aer", n, workers_per_node)
+    return _make(lib().dg_make_aer, n, workers_per_node)
 
 
 def make_static_exponential(n: int) -> MixingSchedule:            # new
-    return _make(lib().dg_make_static_exponential, "static_exponential", n)
+    return _make(lib().dg_make_static_exponential, n)
 
 
 def from_matrices(name: str, workers_per_node: int, rounds: Sequence[np.ndarray]) -> MixingSchedule:
@@ -308,7 +329,7 @@ def from_matrices(name: str, workers_per_node: int, rounds: Sequence[np.ndarray]
     P, n, n2 = mats.shape
     if n != n2:
         raise ConfigError("from_matrices: matrices must be square")
-    return _make(lib().dg_schedule_from_matrices, name, _dptr(mats), n, P, workers_per_node)
+    return _make(lib().dg_schedule_from_matrices_named, name.encode(), _dptr(mats), n, P, workers_per_node)
 
 
 def validate(w) -> MixingValidation:                              # topology.hpp:80
@@ -418,10 +439,33 @@ def fill_synthetic(out, seed: int, purpose: int, worker: int, iteration: int, st
 
 
 # ----------------------------------------------------------------------------- consensus (f2)
-def gossip_consensus(schedule: MixingSchedule, x0: np.ndarray, rounds: int, device: int = 0) -> np.ndarray:
+class ConsensusTrajectory(np.ndarray):
+    """ConsensusTrajectory (topology.hpp:90-96): error[t], t = 0..rounds, as a
+    float64 array (so arithmetic and comparisons work elementwise)."""
+
+    def __new__(cls, error):
+        return np.asarray(error, np.float64).view(cls)
+
+    @property
+    def error(self) -> np.ndarray:
+        return self.view(np.ndarray)
+
+    def to_csv(self, path_or_file) -> None:
+        """Trajectory export, columns `round,consensus_error`."""
+        lines = ["round,consensus_error"] + [f"{t},{e:.17g}" for t, e in enumerate(self.error)]
+        text = "\n".join(lines) + "\n"
+        if hasattr(path_or_file, "write"):
+            path_or_file.write(text)
+        else:
+            with open(path_or_file, "w") as f:
+                f.write(text)
+
+
+def gossip_consensus(schedule: MixingSchedule, x0: np.ndarray, rounds: int, device: int = 0) -> ConsensusTrajectory:
     """gossip_consensus (topology.hpp:90-100) on one GPU:
     x <- W^(t) x for t = 1..rounds on fp32 buckets (fp64 mixing accumulation),
-    error[t] = sum_i ||x_i - xbar||^2 / sum_i ||x_i^0 - xbar||^2; zero initial
+    error[t] = sum_i ||x_i - xbar0||^2 / sum_i ||x_i^0 - xbar0||^2 with xbar0 the
+    preserved initial mean (fixed on the device before round 1); zero initial
     dispersion gives an all-zero trajectory.  The step is the fused engine with
     zero gradients, where DAdam reduces exactly to x <- mix."""
     x0 = np.ascontiguousarray(x0, np.float32)
@@ -435,15 +479,16 @@ def gossip_consensus(schedule: MixingSchedule, x0: np.ndarray, rounds: int, devi
         for i in range(n):
             eng.upload(i, X, x0[i])
         err = np.zeros(rounds + 1)
+        eng.consensus_fix_mean()
         d0, _ = eng.consensus()
         if d0 == 0.0:
-            return err
+            return ConsensusTrajectory(err)
         err[0] = 1.0
         for t in range(1, rounds + 1):
             eng.step(t)
             err[t] = eng.consensus()[0] / d0
         eng.sync()
-        return err
+        return ConsensusTrajectory(err)
     finally:
         eng.close()
 
@@ -508,6 +553,10 @@ class Engine:
         _check(lib().dg_engine_gather(self._h, local, which, idx.ctypes.data_as(_VP), idx.size,
                                       out.ctypes.data_as(_VP)))
         return out
+
+    def consensus_fix_mean(self):
+        """Fix xbar of later consensus() calls to the current mean (collective)."""
+        _check(lib().dg_engine_consensus_fix_mean(self._h))
 
     def consensus(self):
         """(sum_i ||x_i - xbar||^2, ||xbar||^2) over all nodes; collective across ranks."""

@@ -52,6 +52,7 @@ struct Round {
 struct dg_schedule {
   int n = 0;
   int wpn = 1;
+  std::string name;  // MixingSchedule::name() (topology.hpp:50)
   std::vector<dg::Round> rounds;
   const dg::Round& at(long round) const;  // 1-based periodic; throws ConfigError
 };

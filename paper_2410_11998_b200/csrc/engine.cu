@@ -411,6 +411,81 @@ void launch_tma(const RoundPlan& p, const Buffers& bf, int algo, bool fold, size
     launch_tma_t<1, false>(a, ns_max, smem, units, st);
 }
 
+// ------------------------------------------------------------------ staged launch (default K1)
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+// DG_STAGED: 1 (default) the shared-memory staged kernel wherever the round
+// fits it, 0 the register-streaming kernels (round-1 paths, kept for sweeps)
+bool staged_enabled() {
+  static const bool v = env_int("DG_STAGED", 1) != 0;
+  return v;
+}
+bool staged_fits(const RoundPlan& p) {
+  return p.n_local <= kStMaxNodes && p.n_local + int(p.recv_node.size()) <= kStMaxRows &&
+         p.max_deg <= kMaxDegDev;
+}
+
+template <int ALGO, bool FOLD, int S>
+void launch_staged_t(const StagedArgs& a, size_t smem, int sms, cudaStream_t st) {
+  auto kern = gossip_adam_staged<ALGO, FOLD, S>;
+  static bool configured = false;
+  if (!configured) {
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+               "staged smem attribute");
+    configured = true;
+  }
+  const int threads = 32 * a.nl;
+  static std::map<std::pair<int, size_t>, int> occ_cache;
+  int& occ = occ_cache[{threads, smem}];
+  if (!occ) {
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem), "staged occupancy");
+    occ = std::max(1, occ);
+  }
+  const long long tw = 32LL << a.tw_shift;
+  const long long tiles = std::max(1LL, ((a.n >> 2) + tw - 1) / tw);
+  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * sms));
+  kern<<<unsigned(std::min(tiles, resident)), threads, smem, st>>>(a);
+}
+
+// S-deep ring of tiles of 32 << tw_shift float4 columns; DG_ST_STAGES (default
+// 3) and DG_ST_TW (default 32 float4 columns) are tuning knobs, reduced when a
+// round's staged rows do not fit 227 KB of shared memory.
+void launch_staged(const StagedArgs& a, int algo, bool fold, int sms, cudaStream_t st) {
+  static const int want_s = std::max(2, std::min(4, env_int("DG_ST_STAGES", 3)));
+  static const int want_shift = [] {
+    const int tw = std::max(32, env_int("DG_ST_TW", 32));
+    int sh = 0;
+    while ((32 << (sh + 1)) <= tw && sh < 3) ++sh;
+    return sh;
+  }();
+  StagedArgs b = a;
+  const int K = algo == DG_ALGO_ACCUM ? 4 : 3;
+  const size_t row_bytes = 16;
+  int S = want_s, sh = want_shift;
+  auto smem_of = [&](int s_, int sh_) { return size_t(s_) * (b.nx + K * b.nl) * (size_t(32) << sh_) * row_bytes; };
+  while (smem_of(S, sh) > 227 * 1024 && sh > 0) --sh;
+  while (smem_of(S, sh) > 227 * 1024 && S > 2) --S;
+  if (smem_of(S, sh) > 227 * 1024) config_error("staged: round does not fit shared memory");
+  b.tw_shift = sh;
+  const size_t smem = smem_of(S, sh);
+#define DG_ST_CASE(A, F)                                              \
+  switch (S) {                                                        \
+    case 2: return launch_staged_t<A, F, 2>(b, smem, sms, st);        \
+    case 3: return launch_staged_t<A, F, 3>(b, smem, sms, st);        \
+    default: return launch_staged_t<A, F, 4>(b, smem, sms, st);       \
+  }
+  if (algo == DG_ALGO_DADAM) {
+    DG_ST_CASE(0, false)
+  } else if (fold) {
+    DG_ST_CASE(1, true)
+  } else {
+    DG_ST_CASE(1, false)
+  }
+#undef DG_ST_CASE
+}
+
 }  // namespace
 }  // namespace dg
 
@@ -436,6 +511,8 @@ struct dg_engine {
   long launches = 0, steps = 0;
   double sent = 0, received = 0, hbm = 0;
   std::vector<unsigned char> argbuf;
+  bool staged = false;  // shared-memory staged kernel for every round (decided globally)
+  dg::StagedArgs sargs;
   // optional per-launch CUDA-event timing (bench roofline)
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
@@ -459,6 +536,7 @@ struct dg_engine {
   void step_range(long t, size_t off, size_t len);
   // All-Reduce Adam (f3)
   double* gsum = nullptr;  // [d_pad] fp64 gradient column sums
+  double* xbar_ref = nullptr;  // fixed fp64 column sums for the consensus error (f2)
   int* inv_flag = nullptr; // first iteration with drifting workers (INT_MAX = none)
   void step_allreduce(long t, const dg::DevScalars& s);
 
@@ -499,6 +577,13 @@ dg_engine::~dg_engine() {
   if (device >= 0) cudaSetDevice(device);
   if (comp) cudaStreamSynchronize(comp);
   if (comm) cudaStreamSynchronize(comm);
+  // P2P: peers may still be reading this rank's exported x buffers over NVLink
+  // (their last exchange-round kernel); one more stream-ordered barrier before
+  // anything exported is unmapped or freed (destroy is collective)
+  if (transport == DG_TRANSPORT_P2P && G > 1 && nccl && bar_buf && comp) {
+    if (ncclAllReduce(bar_buf, bar_buf, 1, ncclFloat, ncclSum, nccl, comp) == ncclSuccess)
+      cudaStreamSynchronize(comp);
+  }
   if (nccl) ncclCommDestroy(nccl);
   for (float* a : arena)
     if (a) cudaFree(a);
@@ -511,6 +596,7 @@ dg_engine::~dg_engine() {
   if (flag) cudaFree(flag);
   if (inv_flag) cudaFree(inv_flag);
   if (gsum) cudaFree(gsum);
+  if (xbar_ref) cudaFree(xbar_ref);
   if (rbuf) cudaFree(rbuf);
   for (auto& kv : range_ev)
     if (kv.second) cudaEventDestroy(kv.second);
@@ -547,9 +633,33 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
                   : transport == DG_TRANSPORT_P2P ? peer_x(p.recv_node[r]) + off
                                                   : slots + (size_t(slot_set) * max_recv + r) * chunk;
   const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr};
-  const bool tma = dg::use_tma(p);
+  const bool st_k = staged;
+  const bool tma = !st_k && dg::use_tma(p);
   dg::LaunchFn fn = nullptr;
-  if (!tma) {
+  if (st_k) {
+    auto& a = sargs;
+    std::memset(&a, 0, sizeof(a));
+    a.nl = p.n_local;
+    a.nx = p.n_local + int(p.recv_node.size());
+    for (int i = 0; i < p.n_local; ++i) a.xsrc[i] = x[i] + off;
+    for (size_t r = 0; r < p.recv_node.size(); ++r) a.xsrc[p.n_local + r] = slot_ptr[r];
+    for (int i = 0; i < p.n_local; ++i) {
+      a.xo[i] = xo[i] + off;
+      a.g[i] = g[i] + off;
+      a.m[i] = m[i] + off;
+      a.v[i] = v[i] + off;
+      a.b[i] = algo == DG_ALGO_ACCUM ? b[i] + off : nullptr;
+      a.deg[i] = p.deg[i];
+      for (int k = 0; k < p.deg[i]; ++k) {
+        a.src[i][k] = (unsigned char)p.src[i][k];
+        a.w[i][k] = p.w[i][k];
+      }
+    }
+    a.s = s;
+    a.n = (long long)len;
+    a.t = int(t);
+    a.div_flag = flag;
+  } else if (!tma) {
     dg::fill_args(argbuf, p, bf, off, len, s, int(t), flag);
     fn = dg::pick(p.comp_size, dg::launch_ns(p), algo, fold);
   }
@@ -564,7 +674,9 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
                          ? 4.0 * double(len) * double(p.recv_node.size())
                          : 0.0;
   timed(bytes, nvl, [&] {
-    if (tma)
+    if (st_k)
+      dg::launch_staged(sargs, algo, fold, sms_for(p), comp);
+    else if (tma)
       dg::launch_tma(p, bf, algo, fold, off, len, s, int(t), flag, comp);
     else
       fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), sms_for(p), comp);
@@ -832,15 +944,29 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     const int pp_min = e->in_place ? 0 : (ppenv ? std::atoi(ppenv) : 4);
     bool any_pp = false;
     e->round_remote.assign(e->P, 0);
+    // every rank's plan of every round: the staged kernel is used only if it
+    // fits every round on every rank, so all ranks take identical x-buffer decisions
+    std::vector<std::vector<dg::RoundPlan>> all(e->P);
+    e->staged = dg::staged_enabled();
+    for (int r = 0; r < e->P; ++r)
+      for (int g = 0; g < e->G; ++g) {
+        all[r].push_back(g == e->rank ? e->plans[r] : dg::build_round_plan(*c->schedule, e->G, g, r + 1));
+        e->staged = e->staged && dg::staged_fits(all[r].back());
+      }
     for (int r = 0; r < e->P; ++r) {
       bool pp = false;
       for (int g = 0; g < e->G; ++g) {
-        const auto q = g == e->rank ? e->plans[r] : dg::build_round_plan(*c->schedule, e->G, g, r + 1);
-        if ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize) pp = true;
+        const auto& q = all[r][g];
+        if (!e->staged && ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize)) pp = true;
         if (!q.recv_node.empty()) e->round_remote[r] = 1;
       }
       if (p2p && e->round_remote[r]) pp = true;
-      if (pp) {
+      if (pp && e->staged) {
+        // staged kernel: in place on this GPU; only peers' readers (P2P
+        // exchange rounds) need x^(t) in the other buffer
+        e->plans[r].pingpong = true;
+        any_pp = true;
+      } else if (pp) {
         // pair components in P2P exchange rounds keep their structure (each
         // remote source is loaded once per column, in registers) and only
         // redirect x^(t) to the other buffer; otherwise one gather per node
@@ -867,6 +993,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
           if (cp.srcs[k] < 0) ++remote_reads;
       const int ncomp = int(pr.comps.size());
       if (pr.comp_size == 1 && ncomp >= dg::warps_min_nc() && ncomp <= 8) remote_reads = long(pr.recv_node.size());
+      if (e->staged) remote_reads = long(pr.recv_node.size());  // one staged copy per tile
       const char* pv = std::getenv("DG_P2P_PULL");  // 0 never, 1 auto (default), 2 always
       const int pull_mode = pv ? std::atoi(pv) : 1;
       // in-kernel peer loads reach ~770 GB/s, copy-engine pulls ~420 GB/s (measured):
@@ -926,45 +1053,74 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     for (int b = 0; b < 2; ++b) e->peer_base[b].assign(e->G, nullptr);
     e->peer_base[0][e->rank] = e->arena[DG_BUF_X];
     e->peer_base[1][e->rank] = e->x_alt;
-    if (p2p) try {
-      // exchange CUDA IPC handles of both x buffers (one 128-byte record per rank)
+    if (p2p) {
+      // Exchange CUDA IPC handles of both x buffers (one 128-byte record per
+      // rank), open the peers', then AGREE on the outcome (all-reduce min of a
+      // per-rank success flag) so every rank commits to the same transport.
+      // Only CUDA (IPC) failures are tolerated locally; NCCL errors propagate.
       static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
-      std::vector<char> mine(128), all(128 * size_t(e->G));
-      CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data()), e->arena[DG_BUF_X]));
-      CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + 64), e->x_alt));
+      std::vector<char> mine(128, 0), all(128 * size_t(e->G));
+      int ok = 1;
+      std::string why;
+      auto attempt = [&](auto&& f) {
+        if (!ok) return;
+        try {
+          f();
+        } catch (const dg::Error& err) {
+          if (err.code != DG_CUDA_ERROR) throw;
+          ok = 0;
+          why = err.what();
+          cudaGetLastError();
+        }
+      };
+      attempt([&] {
+        CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data()), e->arena[DG_BUF_X]));
+        CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + 64), e->x_alt));
+      });
       char* dbuf = nullptr;
+      int* dok = nullptr;
       CU(cudaMalloc(&dbuf, all.size()));
+      CU(cudaMalloc(&dok, sizeof(int)));
       CU(cudaMemcpy(dbuf + 128 * size_t(e->rank), mine.data(), 128, cudaMemcpyHostToDevice));
       NC(ncclAllGather(dbuf + 128 * size_t(e->rank), dbuf, 128, ncclChar, e->nccl, e->comp));
       CU(cudaStreamSynchronize(e->comp));
       CU(cudaMemcpy(all.data(), dbuf, all.size(), cudaMemcpyDeviceToHost));
-      CU(cudaFree(dbuf));
-      for (int g = 0; g < e->G; ++g) {
-        if (g == e->rank) continue;
-        for (int b = 0; b < 2; ++b) {
-          cudaIpcMemHandle_t h;
-          std::memcpy(&h, all.data() + 128 * size_t(g) + 64 * b, 64);
-          void* ptr = nullptr;
-          CU(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
-          e->peer_base[b][g] = static_cast<float*>(ptr);
-        }
-      }
-      CU(cudaMalloc(&e->bar_buf, sizeof(float)));
-      CU(cudaMemset(e->bar_buf, 0, sizeof(float)));
-    } catch (const dg::Error& err) {
-      // AUTO: no CUDA IPC between these processes -> chunked NCCL send/recv.
-      // (IPC success/failure is a property of the node, identical on all ranks.)
-      if (!auto_transport) throw;
-      cudaGetLastError();
-      for (int g = 0; g < e->G; ++g)
-        for (int b = 0; b < 2; ++b)
-          if (g != e->rank && e->peer_base[b][g]) {
-            cudaIpcCloseMemHandle(e->peer_base[b][g]);
-            e->peer_base[b][g] = nullptr;
+      attempt([&] {
+        for (int g = 0; g < e->G; ++g) {
+          if (g == e->rank) continue;
+          for (int b = 0; b < 2; ++b) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, all.data() + 128 * size_t(g) + 64 * b, 64);
+            void* ptr = nullptr;
+            CU(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            e->peer_base[b][g] = static_cast<float*>(ptr);
           }
-      e->transport = DG_TRANSPORT_NCCL;
-      p2p = false;
-      if (e->max_recv && !e->slots) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
+        }
+      });
+      CU(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+      NC(ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, e->nccl, e->comp));
+      CU(cudaStreamSynchronize(e->comp));
+      CU(cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost));
+      CU(cudaFree(dbuf));
+      CU(cudaFree(dok));
+      if (ok) {
+        CU(cudaMalloc(&e->bar_buf, sizeof(float)));
+        CU(cudaMemset(e->bar_buf, 0, sizeof(float)));
+      } else {
+        for (int g = 0; g < e->G; ++g)
+          for (int b = 0; b < 2; ++b)
+            if (g != e->rank && e->peer_base[b][g]) {
+              cudaIpcCloseMemHandle(e->peer_base[b][g]);
+              e->peer_base[b][g] = nullptr;
+            }
+        // every rank reaches this branch together (agreed flag)
+        if (!auto_transport)
+          dg::config_error("engine_create: P2P transport unavailable (CUDA IPC failed on some rank" +
+                           (why.empty() ? std::string(")") : std::string(": ") + why + ")"));
+        e->transport = DG_TRANSPORT_NCCL;
+        p2p = false;
+        if (e->max_recv && !e->slots) CU(cudaMalloc(&e->slots, sizeof(float) * 2 * e->max_recv * e->chunk));
+      }
     }
     *out = e.release();
   });
@@ -1043,21 +1199,39 @@ int dg_engine_fill_synthetic(dg_engine* e, int which, uint64_t seed, uint32_t pu
   });
 }
 
+// fp64 column sums of the current x over all N nodes (collective), into `colsum`
+static void consensus_colsum(dg_engine* e, double* colsum, const dg::NodePtrs& xp) {
+  const unsigned grid = dg::grid_for((long long)e->d, 8);
+  dg::column_sum<<<grid, 256, 0, e->comp>>>(colsum, xp, e->NL, (long long)e->d);
+  CU(cudaGetLastError());
+  if (e->G > 1) NC(ncclAllReduce(colsum, colsum, e->d, ncclDouble, ncclSum, e->nccl, e->comp));
+}
+
+int dg_engine_consensus_fix_mean(dg_engine* e) {
+  return guarded([&] {
+    if (!e) dg::config_error("engine_consensus_fix_mean: null handle");
+    CU(cudaSetDevice(e->device));
+    dg::NodePtrs xp{};
+    for (int i = 0; i < e->NL; ++i) xp.p[i] = e->buf(DG_BUF_X, i);
+    if (!e->xbar_ref) CU(cudaMalloc(&e->xbar_ref, e->d * sizeof(double)));
+    consensus_colsum(e, e->xbar_ref, xp);
+    CU(cudaStreamSynchronize(e->comp));
+  });
+}
+
 int dg_engine_consensus(dg_engine* e, double* dispersion, double* mean_sq) {
   return guarded([&] {
     if (!e) dg::config_error("engine_consensus: null handle");
     CU(cudaSetDevice(e->device));
     dg::NodePtrs xp{};
     for (int i = 0; i < e->NL; ++i) xp.p[i] = e->buf(DG_BUF_X, i);
-    double* colsum = nullptr;
+    double* colsum = e->xbar_ref;
     double* out = nullptr;
-    CU(cudaMallocAsync(reinterpret_cast<void**>(&colsum), e->d * sizeof(double), e->comp));
+    if (!colsum) CU(cudaMallocAsync(reinterpret_cast<void**>(&colsum), e->d * sizeof(double), e->comp));
     CU(cudaMallocAsync(reinterpret_cast<void**>(&out), 2 * sizeof(double), e->comp));
     CU(cudaMemsetAsync(out, 0, 2 * sizeof(double), e->comp));
     const unsigned grid = dg::grid_for((long long)e->d, 8);
-    dg::column_sum<<<grid, 256, 0, e->comp>>>(colsum, xp, e->NL, (long long)e->d);
-    CU(cudaGetLastError());
-    if (e->G > 1) NC(ncclAllReduce(colsum, colsum, e->d, ncclDouble, ncclSum, e->nccl, e->comp));
+    if (!e->xbar_ref) consensus_colsum(e, colsum, xp);
     // mean term counted once (rank 0); dispersion of the resident nodes on every rank
     dg::dispersion<<<grid, 256, 0, e->comp>>>(out, colsum, 1.0 / double(e->N), xp, e->NL, (long long)e->d,
                                               e->rank == 0);
@@ -1065,7 +1239,7 @@ int dg_engine_consensus(dg_engine* e, double* dispersion, double* mean_sq) {
     if (e->G > 1) NC(ncclAllReduce(out, out, 2, ncclDouble, ncclSum, e->nccl, e->comp));
     double h[2];
     CU(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, e->comp));
-    CU(cudaFreeAsync(colsum, e->comp));
+    if (colsum != e->xbar_ref) CU(cudaFreeAsync(colsum, e->comp));
     CU(cudaFreeAsync(out, e->comp));
     CU(cudaStreamSynchronize(e->comp));
     if (dispersion) *dispersion = h[0];

@@ -10,7 +10,9 @@
 #include <cmath>
 #include <climits>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <string>
 #include <numeric>
 
 #include "dg_internal.hpp"
@@ -95,7 +97,7 @@ std::vector<double> eig_sym(std::vector<double> a, int n) {
 
 // MixingSchedule::from_matrices contract (topology.hpp:36-39): every round
 // passes validate() and the period's union graph is connected.
-dg_schedule* finish(int n, int wpn, std::vector<Round> rounds) {
+dg_schedule* finish(int n, int wpn, std::vector<Round> rounds, const char* name = "custom") {
   if (rounds.empty()) dg::config_error("schedule: empty");
   for (size_t r = 0; r < rounds.size(); ++r) {
     const auto v = dg::validate_dense(
@@ -125,6 +127,7 @@ dg_schedule* finish(int n, int wpn, std::vector<Round> rounds) {
   auto* s = new dg_schedule;
   s->n = n;
   s->wpn = wpn;
+  s->name = name ? name : "";
   s->rounds = std::move(rounds);
   return s;
 }
@@ -361,7 +364,7 @@ int dg_make_complete(int n, dg_schedule** out) {  // topology.hpp:65-66
       std::iota(r.nbr[i].begin(), r.nbr[i].end(), 0);
       r.w[i].assign(n, 1.0 / double(n));
     }
-    return finish(n, 1, {r});
+    return finish(n, 1, {r}, "complete");
   });
 }
 
@@ -371,7 +374,7 @@ int dg_make_one_peer_ring(int n, dg_schedule** out) {  // topology.hpp:67-69
     // round 1: (2k, 2k+1); round 2: (2k+1, 2k+2 mod N)
     Round r1 = matching_round(n, [](int i) { return i ^ 1; });
     Round r2 = matching_round(n, [n](int i) { return (i & 1) ? (i + 1) % n : (i + n - 1) % n; });
-    return finish(n, 1, {r1, r2});
+    return finish(n, 1, {r1, r2}, "one_peer_ring");
   });
 }
 
@@ -380,7 +383,7 @@ int dg_make_one_peer_exponential(int n, dg_schedule** out) {  // topology.hpp:70
     if (n < 2 || !pow2(n)) dg::config_error("make_one_peer_exponential: N must be a power of 2");
     std::vector<Round> rs;
     for (int r = 0; r < log2i(n); ++r) rs.push_back(matching_round(n, [r](int i) { return i ^ (1 << r); }));
-    return finish(n, 1, rs);
+    return finish(n, 1, rs, "one_peer_exponential");
   });
 }
 
@@ -410,7 +413,7 @@ int dg_make_aer(int n, int wpn, dg_schedule** out) {  // topology.hpp:73-78
       }
       rs.push_back(group_round(n, group));
     }
-    return finish(n, wpn, rs);
+    return finish(n, wpn, rs, "aer");
   });
 }
 
@@ -431,11 +434,16 @@ int dg_make_static_exponential(int n, dg_schedule** out) {  // SURVEY.md Appendi
       nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
       r.w[i].assign(nb.size(), 1.0 / double(nb.size()));
     }
-    return finish(n, 1, {r});
+    return finish(n, 1, {r}, "static_exponential");
   });
 }
 
 int dg_schedule_from_matrices(const double* w, int n, int period, int wpn, dg_schedule** out) {
+  return dg_schedule_from_matrices_named("custom", w, n, period, wpn, out);
+}
+
+int dg_schedule_from_matrices_named(const char* name, const double* w, int n, int period, int wpn,
+                                    dg_schedule** out) {
   return make(out, [&] {  // topology.hpp:44-45
     if (!w || n < 1 || period < 1) dg::config_error("from_matrices: bad arguments");
     if (wpn < 1 || n % wpn) dg::config_error("from_matrices: workers_per_node must divide N");
@@ -452,7 +460,8 @@ int dg_schedule_from_matrices(const double* w, int n, int period, int wpn, dg_sc
           }
         }
     }
-    dg_schedule* s = finish(n, wpn, rs);
+    if (!name) dg::config_error("from_matrices: null name");
+    dg_schedule* s = finish(n, wpn, rs, name);
     // finish() validated the positive part; negative entries must also fail
     for (int r = 0; r < period; ++r)
       for (size_t k = 0; k < size_t(n) * n; ++k)
@@ -499,6 +508,47 @@ int dg_schedule_matrix(const dg_schedule* s, long round, double* w) {
 }
 
 void dg_schedule_free(dg_schedule* s) { delete s; }
+
+namespace {
+void copy_out(const std::string& v, char* buf, size_t cap, size_t* len) {
+  if (len) *len = v.size();
+  if (buf && cap) {
+    const size_t k = std::min(cap - 1, v.size());
+    std::memcpy(buf, v.data(), k);
+    buf[k] = '\0';
+  }
+  if (buf && cap <= v.size()) dg::config_error("string: capacity too small");
+}
+}  // namespace
+
+int dg_schedule_name(const dg_schedule* s, char* buf, size_t cap, size_t* len) {  // topology.hpp:50
+  return dg::guarded([&] {
+    if (!s) dg::config_error("schedule: null");
+    copy_out(s->name, buf, cap, len);
+  });
+}
+
+int dg_validation_pass(const dg_validation* v) {  // MixingValidation::pass(), topology.hpp:29-32
+  return v && v->symmetric && v->nonnegative && v->rows_stochastic && v->cols_stochastic &&
+         v->eigenvalues_in_range;
+}
+
+int dg_validation_describe(const dg_validation* v, char* buf, size_t cap, size_t* len) {
+  return dg::guarded([&] {  // MixingValidation::describe(), topology.hpp:33
+    if (!v) dg::config_error("validation: null");
+    auto yn = [](int b) { return b ? "yes" : "NO"; };
+    char tmp[512];
+    std::snprintf(tmp, sizeof(tmp),
+                  "%s: symmetric=%s (max |w_ij - w_ji| %.3g), nonnegative=%s (min entry %.3g), "
+                  "rows_stochastic=%s (max |row sum - 1| %.3g), cols_stochastic=%s (max |col sum - 1| %.3g), "
+                  "eigenvalues_in_range=%s ([%.6g, %.6g] in (-1, 1])",
+                  dg_validation_pass(v) ? "valid" : "INVALID", yn(v->symmetric), v->max_asymmetry,
+                  yn(v->nonnegative), v->min_entry, yn(v->rows_stochastic), v->max_row_error,
+                  yn(v->cols_stochastic), v->max_col_error, yn(v->eigenvalues_in_range), v->min_eigenvalue,
+                  v->max_eigenvalue);
+    copy_out(tmp, buf, cap, len);
+  });
+}
 
 int dg_validate(const double* w, int n, dg_validation* out) {
   return dg::guarded([&] {

@@ -1,4 +1,5 @@
-"""Every fused-kernel path (TMA-staged, cooperative, per-thread) must be
+"""Every fused-kernel path (shared-memory staged = default, TMA-staged,
+cooperative, per-thread) must be
 bit-exact against the oracle's fp32 mirror for every topology; the path is
 chosen by env knobs read once per process, hence one subprocess per path."""
 import os
@@ -13,13 +14,18 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-PATHS = {"default": {},
-         "pingpong_all": {"DG_PINGPONG_MIN_NC": "1"},
-         "tma_all": {"DG_TMA": "2", "DG_PINGPONG_MIN_NC": "0"},
-         "tma_pingpong": {"DG_TMA": "2", "DG_PINGPONG_MIN_NC": "1"},
-         "per_thread_all": {"DG_TMA": "0", "DG_COOP_MIN_NC": "99", "DG_PINGPONG_MIN_NC": "0"},
-         "coop_all": {"DG_TMA": "0", "DG_COOP_MIN_NC": "2", "DG_PINGPONG_MIN_NC": "0"},
-         "warps_all": {"DG_TMA": "0", "DG_PINGPONG_MIN_NC": "1", "DG_WARPS_MIN_NC": "1"}}
+LEGACY = {"DG_STAGED": "0"}
+PATHS = {"default": {},                       # shared-memory staged kernel (S=3, 32-column tiles)
+         "staged_s2": {"DG_ST_STAGES": "2"},
+         "staged_s4_tw128": {"DG_ST_STAGES": "4", "DG_ST_TW": "128"},
+         "staged_tw64": {"DG_ST_TW": "64"},
+         "legacy": {**LEGACY},
+         "pingpong_all": {**LEGACY, "DG_PINGPONG_MIN_NC": "1"},
+         "tma_all": {**LEGACY, "DG_TMA": "2", "DG_PINGPONG_MIN_NC": "0"},
+         "tma_pingpong": {**LEGACY, "DG_TMA": "2", "DG_PINGPONG_MIN_NC": "1"},
+         "per_thread_all": {**LEGACY, "DG_TMA": "0", "DG_COOP_MIN_NC": "99", "DG_PINGPONG_MIN_NC": "0"},
+         "coop_all": {**LEGACY, "DG_TMA": "0", "DG_COOP_MIN_NC": "2", "DG_PINGPONG_MIN_NC": "0"},
+         "warps_all": {**LEGACY, "DG_TMA": "0", "DG_PINGPONG_MIN_NC": "1", "DG_WARPS_MIN_NC": "1"}}
 
 
 @pytest.mark.parametrize("path", sorted(PATHS))

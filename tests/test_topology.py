@@ -175,3 +175,29 @@ def test_gossip_consensus_oracle_properties(oracle):
         assert err[exact_at] <= 1e-12
     s = oracle.make_one_peer_ring(8)
     assert np.all(oracle.gossip_consensus(s, np.ones((8, 4)), 3) == 0)
+
+
+def test_schedule_names_and_describe(dg):
+    # MixingSchedule::name() (topology.hpp:50) and MixingValidation::describe() (topology.hpp:33)
+    assert dg.make_complete(4).name() == "complete"
+    assert dg.make_one_peer_ring(8).name() == "one_peer_ring"
+    assert dg.make_one_peer_exponential(8).name() == "one_peer_exponential"
+    assert dg.make_aer(8, 2).name() == "aer"
+    assert dg.make_static_exponential(8).name() == "static_exponential"
+    s = dg.from_matrices("my ring", 1, [dg.make_one_peer_ring(4).matrix_at(1), dg.make_one_peer_ring(4).matrix_at(2)])
+    assert s.name() == "my ring" and s.period() == 2
+    v = dg.validate(dg.make_complete(4).matrix_at(1))
+    assert v.passed() and v.describe().startswith("valid:")
+    bad = dg.validate(np.array([[0.6, 0.5], [0.4, 0.5]]))
+    assert not bad.passed()
+    txt = bad.describe()
+    assert txt.startswith("INVALID:") and "symmetric=NO" in txt and "rows_stochastic=NO" in txt
+
+
+def test_consensus_trajectory_csv(dg, tmp_path):
+    # trajectory export `round,consensus_error`; host-only part of f2
+    tr = dg.ConsensusTrajectory([1.0, 0.25, 0.0])
+    assert np.all(tr == np.array([1.0, 0.25, 0.0])) and tr.error.dtype == np.float64
+    path = tmp_path / "c.csv"
+    tr.to_csv(str(path))
+    assert path.read_text().splitlines() == ["round,consensus_error", "0,1", "1,0.25", "2,0"]
