@@ -14,11 +14,16 @@ has been accumulated, the hook hands the bucket to dg_engine_step_range:
     post the bucket's round-(t+1) exchange                   C_k
 
 so the gossip of bucket k overlaps the rest of backward and the next forward.
-The next forward joins the engine's stream.  No optimizer is needed: the engine
-performs the DAdam / AccumAdam update.
+Buckets launch in a fixed global order (bucket 0, 1, ... on every rank) however
+autograd orders the hooks.  An iteration starts with the first hook of a
+backward and ends at the next forward (which joins the engine's stream);
+eval / no_grad forwards never step, and no_sync() accumulates gradients over
+several backwards.  No optimizer is needed: the engine performs the DAdam /
+AccumAdam update.
 """
 from __future__ import annotations
 
+from contextlib import contextmanager
 from typing import Callable, List, Optional
 
 import torch
@@ -115,46 +120,94 @@ class DecentralizedDataParallel(torch.nn.Module):
             for p in ps:
                 self._bucket_of[id(p)] = b
                 p.register_post_accumulate_grad_hook(self._on_grad)
-        self.t = 0
+        self.t = 0                       # iterations whose step has been issued (or is in flight)
+        self._active = False             # a backward of iteration t is firing hooks
+        self._sync = True                # False inside no_sync(): accumulate, no step
+        self._zero_next = False          # g was consumed by a step: zero before the next accumulation
         self._pending = [len(b[2]) for b in self.buckets]
-        self._fired = [True] * len(self.buckets)
+        self._ready = [False] * len(self.buckets)
+        self._next = 0                   # next bucket to launch (fixed global order 0, 1, ...)
+        self._views = {id(p): self._g[o:o + p.numel()].view_as(p) for p, o in self._layout}
 
     # ------------------------------------------------------------------ hooks
     def _on_grad(self, p: torch.Tensor):
+        view = self._views[id(p)]
+        if p.grad is None or p.grad.data_ptr() != view.data_ptr():
+            # zero_grad(set_to_none=True) or a rebound .grad detached the
+            # parameter from the engine's g bucket: copy the fresh gradient back
+            # into the bucket and re-attach the view
+            with torch.no_grad():
+                if p.grad is None:
+                    view.zero_()
+                else:
+                    view.copy_(p.grad)
+            p.grad = view
+        if not self._sync:
+            return
+        if not self._active:             # first hook of a backward: iteration t+1 begins
+            self._active = True
+            self.t += 1
+            self._pending = [len(b[2]) for b in self.buckets]
+            self._ready = [False] * len(self.buckets)
+            self._next = 0
         b = self._bucket_of[id(p)]
         self._pending[b] -= 1
         if self._pending[b] == 0:
-            self._launch(b)
+            self._ready[b] = True
+            self._drain()
+
+    def _drain(self):
+        # Buckets launch strictly in index order on every rank (the exchange is
+        # NCCL point-to-point, matched by issue order), like
+        # torch DDP's next_bucket_: a bucket that becomes ready early waits for
+        # its predecessors.
+        while self._next < len(self.buckets) and self._ready[self._next]:
+            self._launch(self._next)
+            self._next += 1
 
     def _launch(self, b: int):
         start, end, _ = self.buckets[b]
         self.engine.wait_stream(torch.cuda.current_stream())   # g of this bucket is complete
         self.engine.step_range(self.t, start, min(end, self.d) - start)
-        self._fired[b] = True
 
     def finish_iteration(self):
-        """Update buckets whose gradients never arrived (unused parameters), then
-        make the current stream wait for all bucket updates of this iteration."""
-        for b, fired in enumerate(self._fired):
-            if not fired:
-                self._launch(b)
+        """Launch the buckets of the running iteration that have not launched yet
+        (unused parameters never fire hooks), in order, then make the current
+        stream wait for every bucket update of the iteration."""
+        if self._active:
+            for b in range(self.buckets.__len__()):
+                self._ready[b] = True
+            self._drain()
+            self._active = False
+            self._zero_next = True
         self.engine.join(torch.cuda.current_stream())
 
+    @contextmanager
+    def no_sync(self):
+        """Gradient accumulation: backward passes inside accumulate into the
+        engine's g bucket without stepping; the first backward outside steps."""
+        old, self._sync = self._sync, False
+        try:
+            yield
+        finally:
+            self._sync = old
+
     def forward(self, *args, **kwargs):
-        if self.t > 0:
-            self.finish_iteration()
-        self.t += 1
-        self._pending = [len(b[2]) for b in self.buckets]
-        self._fired = [False] * len(self.buckets)
-        with torch.no_grad():
-            self._g.zero_()
+        # A backward that fired hooks since the last forward completed an
+        # iteration: finish it (x^(t) must be final before this forward reads
+        # it).  Evaluation / no_grad forwards and forwards inside no_sync()
+        # never start a step.
+        self.finish_iteration()
+        if self._zero_next and self.training and torch.is_grad_enabled():
+            with torch.no_grad():
+                self._g.zero_()
+            self._zero_next = False
         return self.module(*args, **kwargs)
 
     def synchronize(self):
         """Finish the current iteration and wait for every queued update (raises
         DivergenceError(t) on a non-finite state)."""
-        if self.t > 0:
-            self.finish_iteration()
+        self.finish_iteration()
         self.engine.sync()
 
     def flat_parameters(self) -> torch.Tensor:

@@ -74,3 +74,44 @@ def test_ddp_single_gpu_matches_reference(dg):
     want = ref.x.cpu().numpy()
     assert normwise(got, want) <= 1e-6
     assert loss.item() < 2.5
+
+
+def test_ddp_eval_no_sync_and_zero_grad(dg):
+    """eval / no_grad forwards never step; no_sync() accumulates two
+    backwards into one step; zero_grad(set_to_none=True) re-attaches the
+    gradient to the engine's bucket (compared with the plain-PyTorch reference)."""
+    import copy
+    from ddp_reference import ReferenceDAdam
+    from paper_2410_11998_b200.ddp import DecentralizedDataParallel
+    torch.backends.cuda.matmul.allow_tf32 = False
+    model = _mlp()
+    ref_model = copy.deepcopy(model)
+    cfg = dg.OptimizerConfig(alpha=1e-3, beta1=0.9, beta2=0.999, eps=1e-8)
+    ddp = DecentralizedDataParallel(model, optimizer=cfg, bucket_cap_mb=0.1)
+    names = {id(p): n for n, p in ddp.module.named_parameters()}
+    layout = [((names[id(p)], p.numel()), o) for p, o in ddp._layout]
+    ref = ReferenceDAdam(ref_model, layout, ddp.d, ddp.schedule, cfg, 1, 0)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    batch = lambda: (torch.randn(32, 64, device="cuda", generator=gen), torch.randint(0, 10, (32,), device="cuda", generator=gen))
+    ce = torch.nn.functional.cross_entropy
+    x0 = ddp.flat_parameters().clone()
+    ddp.eval()
+    with torch.no_grad():
+        for _ in range(3):
+            ddp(batch()[0])
+    ddp.synchronize()
+    assert ddp.t == 0 and torch.equal(ddp.flat_parameters(), x0)
+    ddp.train()
+    for it in range(4):
+        (x1, y1), (x2, y2) = batch(), batch()
+        with ddp.no_sync():
+            ce(ddp(x1), y1).backward()
+        ce(ddp(x2), y2).backward()
+        ref.step(lambda m: ce(m(x1), y1) + ce(m(x2), y2))
+        if it == 1:
+            ddp.module.zero_grad(set_to_none=True)
+            ddp.synchronize()
+            # the step of iteration 2 already consumed g; the next accumulation re-binds the views
+    ddp.synchronize()
+    assert ddp.t == 4
+    assert normwise(ddp.flat_parameters().cpu().numpy(), ref.x.cpu().numpy()) <= 1e-6
