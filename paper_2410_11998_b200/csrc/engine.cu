@@ -20,7 +20,7 @@
 #include "dg_internal.hpp"
 #include "kernels.cuh"
 #include "launch.hpp"
-#include "staged.cuh"
+#include "xshare.cuh"
 
 namespace dg {
 namespace {
@@ -107,75 +107,118 @@ int* semantic_flag() {
   return static_cast<int*>(p);
 }
 
-// ------------------------------------------------------------------ staged launch (default K1)
-// DG_STAGED: 1 (default) the shared-memory staged kernel wherever the round
-// fits it, 0 the register-streaming kernels (round-1 paths, kept for sweeps)
-bool staged_enabled() {
-  static const bool v = env_int("DG_STAGED", 1) != 0;
+// ------------------------------------------------------------------ x-sharing launch (default K1)
+// DG_XSHARE: 1 (default) the x-sharing kernel (xshare.cuh) wherever every
+// round fits it, 0 the register-streaming kernels of legacy.cu (round-1
+// paths, kept for sweeps and for rounds with > 8 members, sources or
+// neighbours per mixing component).
+bool xshare_enabled() {
+  static const bool v = env_int("DG_XSHARE", 1) != 0;
   return v;
 }
-bool staged_fits(const RoundPlan& p) {
-  return p.n_local <= kStMaxNodes && p.n_local + int(p.recv_node.size()) <= kStMaxRows &&
-         p.max_deg <= kMaxDegDev;
+// DG_PREFETCH: column blocks (32 float4 columns, 512 B per stream) the
+// x-sharing kernel prefetches into L2 ahead of use (default 1, 0 = off)
+int xshare_prefetch() {
+  static const int v = std::max(0, std::min(64, env_int("DG_PREFETCH", 1)));
+  return v;
 }
 
-template <int ALGO, bool FOLD, int S>
-void launch_staged_t(const StagedArgs& a, size_t smem, int sms, cudaStream_t st) {
-  auto kern = gossip_adam_staged<ALGO, FOLD, S>;
-  static bool configured = false;
-  if (!configured) {
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
-               "staged smem attribute");
-    configured = true;
+// Host image of one round's groups: whole mixing components packed first-fit
+// into groups of <= 8 members and <= 8 source rows (rows of different
+// components are never shared, so a member's sum only sees its own
+// component's rows, ascending global id).
+struct GroupPlan {
+  struct Group {
+    std::vector<int> members;           // resident node indices
+    std::vector<int> srcs;              // rows: >= 0 resident node index, < 0 recv slot -(r+1)
+    std::vector<std::vector<double>> w; // [member][row]
+  };
+  bool ok = false;
+  bool colw = true;  // every source row is read with one weight by all its readers
+  int max_deg = 0;
+  std::vector<Group> groups;
+};
+
+GroupPlan build_group_plan(const RoundPlan& p) {
+  GroupPlan gp;
+  for (const auto& c : p.comps) {
+    const int cm = int(c.members.size()), cs = int(c.srcs.size());
+    if (cm > kShNodes || cs > kShRows) return gp;  // ok = false
+    if (gp.groups.empty() || int(gp.groups.back().members.size()) + cm > kShNodes ||
+        int(gp.groups.back().srcs.size()) + cs > kShRows)
+      gp.groups.emplace_back();
+    auto& g = gp.groups.back();
+    const int r0 = int(g.srcs.size());
+    for (auto& row : g.w) row.resize(r0 + cs, 0.0);
+    g.srcs.insert(g.srcs.end(), c.srcs.begin(), c.srcs.end());
+    for (int jm = 0; jm < cm; ++jm) {
+      g.members.push_back(c.members[jm]);
+      std::vector<double> row(r0 + cs, 0.0);
+      int deg = 0;
+      for (int k = 0; k < cs; ++k) {
+        row[r0 + k] = c.w[jm][k];
+        deg += c.w[jm][k] != 0.0;
+      }
+      if (deg > kShDeg) return gp;
+      gp.max_deg = std::max(gp.max_deg, deg);
+      g.w.push_back(row);
+    }
+    for (int k = 0; k < cs; ++k) {  // column-uniform weights?
+      double wk = 0.0;
+      for (int jm = 0; jm < cm; ++jm) {
+        const double x = c.w[jm][k];
+        if (x == 0.0) continue;
+        if (wk == 0.0) wk = x;
+        else if (x != wk) gp.colw = false;
+      }
+    }
   }
-  const int threads = 32 * a.nl;
-  static std::map<std::pair<int, size_t>, int> occ_cache;
-  int& occ = occ_cache[{threads, smem}];
+  gp.ok = !gp.groups.empty();
+  return gp;
+}
+
+template <int DEG, int ALGO, bool FOLD, bool COLW>
+void launch_xshare_t(const ShArgs& a, int ngroups, int warps, int sms, cudaStream_t st) {
+  auto kern = gossip_adam_xshare<DEG, ALGO, FOLD, COLW>;
+  static std::map<int, int> occ_of;  // resident CTAs per SM by CTA size
+  int& occ = occ_of[warps];
   if (!occ) {
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem), "staged occupancy");
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * warps, 0), "xshare occupancy");
     occ = std::max(1, occ);
   }
-  const long long tw = 32LL << a.tw_shift;
-  const long long tiles = std::max(1LL, ((a.n >> 2) + tw - 1) / tw);
-  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * sms));
-  kern<<<unsigned(std::min(tiles, resident)), threads, smem, st>>>(a);
+  const long long blocks = std::max(1LL, ((a.n >> 2) + 31) / 32);
+  const long long resident = std::max(1LL, (long long)(grid_waves() * occ * sms) / ngroups);
+  dim3 grid(unsigned(std::min(blocks, resident)), unsigned(ngroups));
+  kern<<<grid, 32 * warps, 0, st>>>(a);
 }
 
-// S-deep ring of tiles of 32 << tw_shift float4 columns; DG_ST_STAGES (default
-// 3) and DG_ST_TW (default 32 float4 columns) are tuning knobs, reduced when a
-// round's staged rows do not fit 227 KB of shared memory.
-void launch_staged(const StagedArgs& a, int algo, bool fold, int sms, cudaStream_t st) {
-  static const int want_s = std::max(2, std::min(4, env_int("DG_ST_STAGES", 3)));
-  static const int want_shift = [] {
-    const int tw = std::max(32, env_int("DG_ST_TW", 32));
-    int sh = 0;
-    while ((32 << (sh + 1)) <= tw && sh < 3) ++sh;
-    return sh;
-  }();
-  StagedArgs b = a;
-  const int K = algo == DG_ALGO_ACCUM ? 4 : 3;
-  const size_t row_bytes = 16;
-  int S = want_s, sh = want_shift;
-  auto smem_of = [&](int s_, int sh_) { return 128 + size_t(s_) * (b.nx + K * b.nl) * (size_t(32) << sh_) * row_bytes; };
-  while (smem_of(S, sh) > 227 * 1024 && sh > 0) --sh;
-  while (smem_of(S, sh) > 227 * 1024 && S > 2) --S;
-  if (smem_of(S, sh) > 227 * 1024) config_error("staged: round does not fit shared memory");
-  b.tw_shift = sh;
-  const size_t smem = smem_of(S, sh);
-#define DG_ST_CASE(A, F)                                              \
-  switch (S) {                                                        \
-    case 2: return launch_staged_t<A, F, 2>(b, smem, sms, st);        \
-    case 3: return launch_staged_t<A, F, 3>(b, smem, sms, st);        \
-    default: return launch_staged_t<A, F, 4>(b, smem, sms, st);       \
+void launch_xshare(const ShArgs& a, int ngroups, int warps, int max_deg, bool colw, int algo, bool fold,
+                   int sms, cudaStream_t st) {
+#define DG_XS_C(D, A, F)                                           \
+  if (colw) {                                                      \
+    return launch_xshare_t<D, A, F, true>(a, ngroups, warps, sms, st);  \
+  } else {                                                         \
+    return launch_xshare_t<D, A, F, false>(a, ngroups, warps, sms, st); \
+  }
+#define DG_XS_D(A, F)   \
+  if (max_deg <= 2) {   \
+    DG_XS_C(2, A, F)    \
+  } else if (max_deg <= 4) { \
+    DG_XS_C(4, A, F)    \
+  } else if (max_deg <= 6) { \
+    DG_XS_C(6, A, F)    \
+  } else {              \
+    DG_XS_C(8, A, F)    \
   }
   if (algo == DG_ALGO_DADAM) {
-    DG_ST_CASE(0, false)
+    DG_XS_D(0, false)
   } else if (fold) {
-    DG_ST_CASE(1, true)
+    DG_XS_D(1, true)
   } else {
-    DG_ST_CASE(1, false)
+    DG_XS_D(1, false)
   }
-#undef DG_ST_CASE
+#undef DG_XS_D
+#undef DG_XS_C
 }
 
 }  // namespace
@@ -203,8 +246,12 @@ struct dg_engine {
   long launches = 0, steps = 0;
   double sent = 0, received = 0, hbm = 0;
   std::vector<unsigned char> argbuf;
-  bool staged = false;  // shared-memory staged kernel for every round (decided globally)
-  dg::StagedArgs sargs;
+  bool xshare = false;  // x-sharing kernel for every round (decided globally)
+  std::vector<dg::GroupPlan> gplans;  // per round
+  dg::ShArgs sargs;
+  void launch_groups(const dg::GroupPlan& tp, float* const* x, float* const* xo, const float* const* g,
+                          float* const* m, float* const* v, float* const* b, const float* const* slot_ptr,
+                          size_t off, size_t len, const dg::DevScalars& s, bool fold, long t, int sms);
   // optional per-launch CUDA-event timing (bench roofline)
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
@@ -336,32 +383,14 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
                   : transport == DG_TRANSPORT_P2P ? peer_x(p.recv_node[r]) + off
                                                   : slots + (size_t(slot_set) * max_recv + r) * chunk;
   const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr};
-  const bool st_k = staged;
+  const bool st_k = xshare;
   const bool tma = !st_k && dg::use_tma(p);
   dg::LaunchFn fn = nullptr;
+  const dg::GroupPlan* tp = nullptr;
   if (st_k) {
-    auto& a = sargs;
-    std::memset(&a, 0, sizeof(a));
-    a.nl = p.n_local;
-    a.nx = p.n_local + int(p.recv_node.size());
-    for (int i = 0; i < p.n_local; ++i) a.xsrc[i] = x[i] + off;
-    for (size_t r = 0; r < p.recv_node.size(); ++r) a.xsrc[p.n_local + r] = slot_ptr[r];
-    for (int i = 0; i < p.n_local; ++i) {
-      a.xo[i] = xo[i] + off;
-      a.g[i] = g[i] + off;
-      a.m[i] = m[i] + off;
-      a.v[i] = v[i] + off;
-      a.b[i] = algo == DG_ALGO_ACCUM ? b[i] + off : nullptr;
-      a.deg[i] = p.deg[i];
-      for (int k = 0; k < p.deg[i]; ++k) {
-        a.src[i][k] = (unsigned char)p.src[i][k];
-        a.w[i][k] = p.w[i][k];
-      }
-    }
-    a.s = s;
-    a.n = (long long)len;
-    a.t = int(t);
-    a.div_flag = flag;
+    const size_t ri = size_t(&p - plans.data());
+    if (ri >= gplans.size()) throw dg::Error(DG_INVARIANT, "xshare: plan not owned by the engine");
+    tp = &gplans[ri];
   } else if (!tma) {
     dg::fill_args(argbuf, p, bf, off, len, s, int(t), flag);
     fn = dg::pick(p.comp_size, dg::launch_ns(p), algo, fold);
@@ -378,12 +407,69 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
                          : 0.0;
   timed(bytes, nvl, [&] {
     if (st_k)
-      dg::launch_staged(sargs, algo, fold, sms_for(p), comp);
+      launch_groups(*tp, x, xo, g, m, v, b, slot_ptr, off, len, s, fold, t, sms_for(p));
     else if (tma)
       dg::launch_tma(p, bf, algo, fold, off, len, s, int(t), flag, comp);
     else
       fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), sms_for(p), comp);
   });
+}
+
+// One launch per (up to) kShGroups groups of the round; pointers at offset off.
+void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* const* xo,
+                                   const float* const* g, float* const* m, float* const* v, float* const* b,
+                                   const float* const* slot_ptr, size_t off, size_t len,
+                                   const dg::DevScalars& s, bool fold, long t, int sms) {
+  const int ng = int(tp.groups.size());
+  for (int g0 = 0; g0 < ng; g0 += dg::kShGroups) {
+    auto& a = sargs;
+    std::memset(&a, 0, sizeof(a));
+    const int cnt = std::min(dg::kShGroups, ng - g0);
+    int warps = 1;
+    for (int k = 0; k < cnt; ++k) {
+      const auto& G = tp.groups[size_t(g0 + k)];
+      auto& d = a.grp[k];
+      d.nl = int(G.members.size());
+      d.nx = int(G.srcs.size());
+      warps = std::max(warps, std::max(d.nl, d.nx));  // a warp per member and per source row
+      for (int j = 0; j < d.nx; ++j) {
+        const int c = G.srcs[size_t(j)];
+        d.row[j] = c >= 0 ? x[c] + off : slot_ptr[-c - 1];
+        if (c >= 0 || transport != DG_TRANSPORT_P2P) d.local_rows |= 1u << j;
+        d.wrow[j] = 0.0;
+        for (int q = 0; q < d.nl; ++q)
+          if (G.w[size_t(q)][size_t(j)] != 0.0) d.wrow[j] = G.w[size_t(q)][size_t(j)];
+      }
+      for (int q = 0; q < d.nl; ++q) {
+        const int li = G.members[size_t(q)];
+        d.xo[q] = xo[li] + off;
+        d.g[q] = g[li] + off;
+        d.m[q] = m[li] + off;
+        d.v[q] = v[li] + off;
+        d.b[q] = algo == DG_ALGO_ACCUM ? b[li] + off : nullptr;
+        int k = 0;
+        for (int j = 0; j < d.nx; ++j) {
+          const double wq = G.w[size_t(q)][size_t(j)];
+          if (wq == 0.0) continue;
+          d.src[q][k] = (unsigned char)j;
+          d.w[q][k] = wq;
+          ++k;
+        }
+        d.deg[q] = k;
+        for (; k < dg::kShDeg; ++k) {
+          d.src[q][k] = (unsigned char)dg::kShRows;
+          d.w[q][k] = 0.0;
+        }
+      }
+    }
+    a.s = s;
+    a.n = (long long)len;
+    a.t = int(t);
+    a.prefetch = dg::xshare_prefetch();
+    a.contiguous = dg::env_int("DG_XS_CONTIG", 0) != 0;
+    a.div_flag = flag;
+    dg::launch_xshare(a, cnt, warps, tp.max_deg, tp.colw, algo, fold, sms, comp);
+  }
 }
 
 template <class F>
@@ -653,25 +739,25 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     const int pp_min = e->in_place ? 0 : (ppenv ? std::atoi(ppenv) : 4);
     bool any_pp = false;
     e->round_remote.assign(e->P, 0);
-    // every rank's plan of every round: the staged kernel is used only if it
+    // every rank's plan of every round: the x-sharing kernel is used only if it
     // fits every round on every rank, so all ranks take identical x-buffer decisions
     std::vector<std::vector<dg::RoundPlan>> all(e->P);
-    e->staged = dg::staged_enabled();
+    e->xshare = dg::xshare_enabled();
     for (int r = 0; r < e->P; ++r)
       for (int g = 0; g < e->G; ++g) {
         all[r].push_back(g == e->rank ? e->plans[r] : dg::build_round_plan(*c->schedule, e->G, g, r + 1));
-        e->staged = e->staged && dg::staged_fits(all[r].back());
+        e->xshare = e->xshare && dg::build_group_plan(all[r].back()).ok;
       }
     for (int r = 0; r < e->P; ++r) {
       bool pp = false;
       for (int g = 0; g < e->G; ++g) {
         const auto& q = all[r][g];
-        if (!e->staged && ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize)) pp = true;
+        if (!e->xshare && ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize)) pp = true;
         if (!q.recv_node.empty()) e->round_remote[r] = 1;
       }
       if (p2p && e->round_remote[r]) pp = true;
-      if (pp && e->staged) {
-        // staged kernel: in place on this GPU; only peers' readers (P2P
+      if (pp && e->xshare) {
+        // x-sharing kernel: in place on this GPU; only peers' readers (P2P
         // exchange rounds) need x^(t) in the other buffer
         e->plans[r].pingpong = true;
         any_pp = true;
@@ -702,7 +788,12 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
           if (cp.srcs[k] < 0) ++remote_reads;
       const int ncomp = int(pr.comps.size());
       if (pr.comp_size == 1 && ncomp >= dg::warps_min_nc() && ncomp <= 8) remote_reads = long(pr.recv_node.size());
-      if (e->staged) remote_reads = long(pr.recv_node.size());  // one staged copy per tile
+      if (e->xshare) {  // each group row is loaded once per column
+        e->gplans.push_back(dg::build_group_plan(pr));
+        remote_reads = 0;
+        for (const auto& gr : e->gplans.back().groups)
+          for (int c : gr.srcs) remote_reads += c < 0;
+      }
       const char* pv = std::getenv("DG_P2P_PULL");  // 0 never, 1 auto (default), 2 always
       const int pull_mode = pv ? std::atoi(pv) : 1;
       // in-kernel peer loads reach ~770 GB/s, copy-engine pulls ~420 GB/s (measured):

@@ -1,0 +1,258 @@
+// xshare.cuh -- the default fused gossip + Adam kernel of libdg (sm_100a).
+// Included by engine.cu only (legacy.cu holds the round-1 register-streaming
+// and warp-specialised TMA variants, used when a round does not fit this one).
+//
+// DESIGN.md §3 K1.  A CTA owns a GROUP of whole mixing components (<= 8
+// resident member nodes, <= 8 distinct x^(t-1) source rows); warp w is member
+// w and converter of source row w (a CTA has max(members, rows) warps), and
+// all warps walk the same float4 columns (lane l of every warp on column
+// blockIdx.x*32 + l, grid-stride).  Per column:
+//
+//   1. warp w loads source row w (one 128-bit load per lane), converts the
+//      4 elements to fp64 and, when every reader of the
+//      row uses the same weight w_r (all built-in topologies), multiplies by
+//      w_r ONCE; the 4 doubles go to a double-buffered shared-memory table
+//      P[r][lane].  It also issues its own g, m, v[, acc] loads.
+//   2. __syncthreads (the table is complete; the previous use of the other
+//      buffer ended one barrier ago).
+//   3. warp w sums P[src][lane] over its member's neighbours in ascending
+//      global id (fp64, one rounding -- the oracle's op order, bit-exact),
+//      applies the DAdam / AccumAdam update and stores x^(t), m, v[, acc].
+//
+// So every x element is loaded from HBM (or NVLink) once and converted once
+// however many members mix it; the round-1 warp-per-node kernel converted it
+// once per reader (6x for static exponential), which kept its XU pipe ~45 %
+// busy at the HBM roofline.  Here a thread holds one member's 4-5 float4
+// streams: 3 CTAs of 8 warps per SM.  Lane 0 of every warp bulk-prefetches
+// its streams (cp.async.bulk.prefetch.L2) DG_PREFETCH column blocks ahead,
+// so the demand loads mostly hit L2: the DRAM latency is covered without
+// registers.
+//
+// Jacobi snapshot: every read of a column's x rows (step 1)
+// precedes the barrier, every x^(t) store of that column (step 3) follows it,
+// and only this CTA touches the column of the group's members (components
+// are closed), so x is updated in place.  Remote readers (P2P exchange
+// rounds) need x^(t) in the other buffer: xo[] then points there.
+#pragma once
+#include "kernels.cuh"
+
+namespace dg {
+
+constexpr int kShRows = 8;    // source rows per group
+constexpr int kShNodes = 8;   // member nodes per group (= warps per CTA)
+constexpr int kShDeg = 8;     // neighbours per member (self included)
+constexpr int kShGroups = 8;  // groups per launch (blockIdx.y)
+
+struct ShGroup {
+  const float* row[kShRows];          // x^(t-1) source rows (resident, peer or recv slot)
+  double wrow[kShRows];               // COLW: the weight every reader of row r uses
+  float* xo[kShNodes];                // where member q's x^(t) goes
+  const float* g[kShNodes];
+  float* m[kShNodes];
+  float* v[kShNodes];
+  float* b[kShNodes];                 // AccumAdam accumulator (null for DAdam)
+  double w[kShNodes][kShDeg];         // !COLW: member q's weight on its k-th neighbour
+  unsigned char src[kShNodes][kShDeg];  // member q's k-th neighbour (ascending global id) as a row;
+                                        // kShRows (the zero row) past its degree
+  int deg[kShNodes];
+  int nl, nx;
+  unsigned local_rows;                // bit r: row r is a resident bucket (L2-prefetchable)
+};
+struct ShArgs {
+  ShGroup grp[kShGroups];
+  DevScalars s;
+  long long n;  // elements in this launch
+  int t;
+  int prefetch;    // column blocks prefetched into L2 ahead of use (DG_PREFETCH)
+  int contiguous;  // 1: one contiguous range of column blocks per CTA (DG_XS_CONTIG)
+  int* div_flag;
+};
+
+// P table: [2 buffers][kShRows + 1][2 component pairs][32 lanes] double2 (a
+// warp's 128-bit accesses touch 512 consecutive bytes: conflict-free).  Row
+// kShRows is all zeros: members with fewer than DEG neighbours pad their list
+// with it (acc + 0.0 == acc exactly, acc starting at +0 can never be -0).
+constexpr int kShRowD2 = 2 * 32;                    // double2 per row
+constexpr int kShBufD2 = (kShRows + 1) * kShRowD2;  // double2 per buffer
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+#ifndef DG_XS_MINB
+#define DG_XS_MINB 3  // resident CTAs per SM the register budget is sized for
+#endif
+template <int DEG, int ALGO, bool FOLD, bool COLW>
+__global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(const __grid_constant__ ShArgs a) {
+  __shared__ double2 P[2 * kShBufD2];
+  const ShGroup& gp = a.grp[blockIdx.y];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nl = gp.nl, nx = gp.nx;
+  const bool member = w < nl;  // warp w updates member w ...
+  const bool conv = w < nx;    // ... and converts source row w
+  const long long n4 = a.n >> 2;
+  // column blocks of this CTA: blk = first + i * step, i < count -- grid-stride
+  // (default: at any moment the CTAs sweep one compact window of every
+  // stream, so DRAM rows are used whole) or one contiguous range per CTA
+  const long long nblk = (n4 + 31) >> 5;
+  long long first, step, count;
+  if (a.contiguous) {
+    const long long per = (nblk + gridDim.x - 1) / gridDim.x;
+    first = (long long)blockIdx.x * per;
+    step = 1;
+    count = max(0LL, min(nblk, first + per) - first);
+  } else {
+    first = blockIdx.x;
+    step = gridDim.x;
+    count = blockIdx.x < nblk ? (nblk - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  }
+  const float* xr = conv ? gp.row[w] : nullptr;
+  const double wr = conv && COLW ? gp.wrow[w] : 1.0;
+  const bool pf_x = conv && (gp.local_rows >> w & 1);  // resident row: prefetchable into L2
+  const float* gq = member ? gp.g[w] : nullptr;
+  float* xq = member ? gp.xo[w] : nullptr;
+  float* mq = member ? gp.m[w] : nullptr;
+  float* vq = member ? gp.v[w] : nullptr;
+  float* bq = member ? gp.b[w] : nullptr;
+  // member w's neighbour rows (ascending global id, zero row padded) as
+  // double2 offsets into a buffer, and (!COLW) the weights
+  int soff[DEG];
+  double wk[COLW ? 1 : DEG];
+#pragma unroll
+  for (int k = 0; k < DEG; ++k) {
+    soff[k] = (member ? gp.src[w][k] : kShRows) * kShRowD2 + lane;
+    if (!COLW) wk[k] = member ? gp.w[w][k] : 0.0;
+  }
+  if (threadIdx.x < 2 * kShRowD2) {  // the zero rows of both buffers
+    const int b = threadIdx.x / kShRowD2, i = threadIdx.x % kShRowD2;
+    P[b * kShBufD2 + kShRows * kShRowD2 + i] = make_double2(0.0, 0.0);
+  }
+  // lane 0: bulk L2 prefetch of this warp's streams for column block blk
+  const int pd = a.prefetch;
+  auto prefetch = [&](long long i) {
+    if (lane != 0 || i >= count) return;
+    const long long e = (first + i * step) << 7;  // first element of the block
+    const uint32_t bytes = uint32_t(min(128LL, ((a.n - e) + 3) & ~3LL)) * 4u;
+    if (member) {
+      prefetch_l2(gq + e, bytes);
+      prefetch_l2(mq + e, bytes);
+      prefetch_l2(vq + e, bytes);
+      if (ALGO == 1) prefetch_l2(bq + e, bytes);
+    }
+    if (pf_x) prefetch_l2(xr + e, bytes);
+  };
+  for (int i = 0; i < pd; ++i) prefetch(i);
+  bool bad = false;
+  int buf = 0;
+  for (long long i = 0; i < count; ++i, buf ^= 1) {
+    prefetch(i + pd);
+    const long long q = ((first + i * step) << 5) + lane;
+    const bool live = q < n4;  // false only for lanes of the last column block
+    const long long e = q << 2;
+    float4 g, m, v, bb;
+    if (member && live) {
+      g = ld_stream(gq + e);
+      m = ld4(mq + e);
+      v = ld4(vq + e);
+      if (ALGO == 1) bb = ld4(bq + e);
+    }
+    double2* Pb = P + buf * kShBufD2;
+    if (conv) {
+      const float4 x = live ? ld4(xr + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      double2 lo, hi;
+      if (COLW) {
+        lo = make_double2(__dmul_rn(wr, double(x.x)), __dmul_rn(wr, double(x.y)));
+        hi = make_double2(__dmul_rn(wr, double(x.z)), __dmul_rn(wr, double(x.w)));
+      } else {
+        lo = make_double2(double(x.x), double(x.y));
+        hi = make_double2(double(x.z), double(x.w));
+      }
+      Pb[w * kShRowD2 + lane] = lo;
+      Pb[w * kShRowD2 + 32 + lane] = hi;
+    }
+    __syncthreads();  // table complete; the other buffer's readers are one barrier back
+    if (member && live) {
+      double ax = 0.0, ay = 0.0, az = 0.0, aw = 0.0;
+#pragma unroll
+      for (int k = 0; k < DEG; ++k) {
+        const double2 lo = Pb[soff[k]], hi = Pb[soff[k] + 32];
+        if (COLW) {
+          ax = __dadd_rn(ax, lo.x);
+          ay = __dadd_rn(ay, lo.y);
+          az = __dadd_rn(az, hi.x);
+          aw = __dadd_rn(aw, hi.y);
+        } else {
+          ax = __dadd_rn(ax, __dmul_rn(wk[k], lo.x));
+          ay = __dadd_rn(ay, __dmul_rn(wk[k], lo.y));
+          az = __dadd_rn(az, __dmul_rn(wk[k], hi.x));
+          aw = __dadd_rn(aw, __dmul_rn(wk[k], hi.y));
+        }
+      }
+      const float4 mx = make_float4(__double2float_rn(ax), __double2float_rn(ay), __double2float_rn(az),
+                                    __double2float_rn(aw));
+      float4 x;
+      if (ALGO == 0) {
+        bool ok = dadam_elem(mx.x, g.x, x.x, m.x, v.x, a.s);
+        ok &= dadam_elem(mx.y, g.y, x.y, m.y, v.y, a.s);
+        ok &= dadam_elem(mx.z, g.z, x.z, m.z, v.z, a.s);
+        ok &= dadam_elem(mx.w, g.w, x.w, m.w, v.w, a.s);
+        bad |= !ok;
+        st4(xq + e, x);
+        st4_mv(mq + e, m);
+        st4_mv(vq + e, v);
+      } else {
+        bool ok = accum_elem<FOLD>(mx.x, g.x, x.x, m.x, v.x, bb.x, a.s);
+        ok &= accum_elem<FOLD>(mx.y, g.y, x.y, m.y, v.y, bb.y, a.s);
+        ok &= accum_elem<FOLD>(mx.z, g.z, x.z, m.z, v.z, bb.z, a.s);
+        ok &= accum_elem<FOLD>(mx.w, g.w, x.w, m.w, v.w, bb.w, a.s);
+        bad |= !ok;
+        st4(xq + e, x);
+        st4_mv(bq + e, bb);
+        if (FOLD) {
+          st4_mv(mq + e, m);
+          st4_mv(vq + e, v);
+        }
+      }
+    }
+  }
+  // scalar tail (n % 4 elements): CTA 0, lane l of member warp w takes element
+  // n4*4 + l; all x reads precede the barrier, all writes follow it
+  const long long tail0 = n4 << 2;
+  if (blockIdx.x == 0 && tail0 < a.n) {
+    __syncthreads();  // the last column block's table reads are done
+    const long long e = tail0 + lane;
+    const bool t_live = lane < a.n - tail0;
+    if (conv) {
+      const double xe = t_live ? double(xr[e]) : 0.0;
+      P[w * kShRowD2 + lane] = make_double2(COLW ? __dmul_rn(wr, xe) : xe, 0.0);
+    }
+    __syncthreads();
+    if (member && t_live) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < DEG; ++k) {
+        const double p = P[soff[k]].x;
+        acc = COLW ? __dadd_rn(acc, p) : __dadd_rn(acc, __dmul_rn(wk[k], p));
+      }
+      const float mx = __double2float_rn(acc);
+      float x, m = mq[e], v = vq[e];
+      if (ALGO == 0) {
+        bad |= !dadam_elem(mx, gq[e], x, m, v, a.s);
+        mq[e] = m;
+        vq[e] = v;
+      } else {
+        float b = bq[e];
+        bad |= !accum_elem<FOLD>(mx, gq[e], x, m, v, b, a.s);
+        bq[e] = b;
+        if (FOLD) {
+          mq[e] = m;
+          vq[e] = v;
+        }
+      }
+      xq[e] = x;
+    }
+  }
+  report_divergence(bad, a.t, a.div_flag);
+}
+
+}  // namespace dg

@@ -1,5 +1,5 @@
-"""Every fused-kernel path (shared-memory staged = default, TMA-staged,
-cooperative, per-thread) must be
+"""Every fused-kernel path (x-sharing kernel = default, the legacy
+warp-specialised TMA, cooperative, per-thread and warp-per-node kernels) must be
 bit-exact against the oracle's fp32 mirror for every topology; the path is
 chosen by env knobs read once per process, hence one subprocess per path."""
 import os
@@ -14,11 +14,9 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LEGACY = {"DG_STAGED": "0"}
-PATHS = {"default": {},                       # shared-memory staged kernel (S=3, 32-column tiles)
-         "staged_s2": {"DG_ST_STAGES": "2"},
-         "staged_s4_tw128": {"DG_ST_STAGES": "4", "DG_ST_TW": "128"},
-         "staged_tw64": {"DG_ST_TW": "64"},
+LEGACY = {"DG_XSHARE": "0"}
+PATHS = {"default": {},                       # x-sharing kernel
+         "xshare_small_grid": {"DG_WAVES": "0.3"},
          "legacy": {**LEGACY},
          "pingpong_all": {**LEGACY, "DG_PINGPONG_MIN_NC": "1"},
          "tma_all": {**LEGACY, "DG_TMA": "2", "DG_PINGPONG_MIN_NC": "0"},
