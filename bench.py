@@ -4,14 +4,19 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-Workload (config.workload): BASELINE.json configs[1]/[4] -- one-peer exponential
-gossip, 8 simulated nodes per B200 (8*N nodes total; N=1 is configs[1] with 8
-nodes on one device, N=8 is configs[4]), 125M-parameter flat fp32 bucket per
-node, DAdam (alpha 2e-3, betas 0.974/0.999).  A "step" is one
-dg_engine_step(t) over every resident node's full bucket: mixing with the
-round-t peers (NCCL send/recv over NVLink for remote peers), Adam moments and
-the model update, in one fused sm_100a kernel per chunk.  Weak scaling: per-GPU
-work is fixed as N grows.
+Workload (config.workload), numbered as BASELINE.md / SURVEY.md (1-5 =
+BASELINE.json configs[0..4]); --config picks one, the default is
+  N = 1: config 3 -- 8 simulated nodes on one B200, static exponential graph,
+          350M-param flat fp32 bucket per node, DAdam (alpha 2e-3, betas
+          0.974/0.999): the largest BASELINE config that fits
+          one GPU (56 GB);
+  N > 1: config 4 -- 8 nodes, alternating (AER) topology, 1.3B-param bucket,
+          AccumAdam s=4, the config BASELINE names for 2/4/8-GPU
+          scaling (208 GB: does not fit one GPU); strong scaling, nodes
+          block-partitioned over the N GPUs.
+A "step" is one dg_engine_step(t) over every resident node's full bucket:
+mixing with the round-t peers (remote x^(t-1) read in-kernel over NVLink),
+Adam moments and the model update, in one fused sm_100a kernel launch.
 
 Prints ONE JSON line on rank 0.
 """
@@ -41,11 +46,14 @@ def parse():
     p.add_argument("--steps", type=int, default=60)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--nodes-per-gpu", type=int, default=8)
-    p.add_argument("--bucket-params", dest="d", type=int, default=125_000_000)
-    p.add_argument("--topology", default="one_peer_exponential",
+    p.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5], default=None,
+                   help="BASELINE config (1-based); default 3 at N=1, 4 at N>1")
+    p.add_argument("--nodes", type=int, default=None, help="total nodes (overrides the config)")
+    p.add_argument("--nodes-per-gpu", type=int, default=None, help="weak scaling: nodes per GPU")
+    p.add_argument("--bucket-params", dest="d", type=int, default=None)
+    p.add_argument("--topology", default=None,
                    choices=["one_peer_exponential", "one_peer_ring", "static_exponential", "aer"])
-    p.add_argument("--algo", choices=["dadam", "accum", "allreduce"], default="dadam")
+    p.add_argument("--algo", choices=["dadam", "accum", "allreduce"], default=None)
     p.add_argument("--chunk", type=int, default=0)
     p.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
     p.add_argument("--e2e-steps", type=int, default=4)
@@ -53,6 +61,43 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
+
+
+# BASELINE.json configs (numbered 1-5 as in BASELINE.md / SURVEY.md)
+CONFIGS = {
+    1: dict(topology="one_peer_ring", nodes=8, d=1 << 20, algo="accum",
+            text="config 1: 8 simulated nodes, ring, 1M-param bucket, AccumAdam s=4"),
+    2: dict(topology="one_peer_exponential", nodes=8, d=125_000_000, algo="dadam",
+            text="config 2: 8 nodes, one-peer exponential, 125M-param bucket (GPT-2 small size), DAdam"),
+    3: dict(topology="static_exponential", nodes=8, d=350_000_000, algo="dadam",
+            text="config 3: 8 nodes, static exponential, 350M-param bucket, DAdam"),
+    4: dict(topology="aer", nodes=8, d=1_300_000_000, algo="accum",
+            text="config 4: 8 nodes, alternating (AER) topology, 1.3B-param bucket, AccumAdam s=4"),
+    5: dict(topology="one_peer_exponential", nodes=64, d=125_000_000, algo="dadam",
+            text="config 5: 64 simulated nodes, one-peer exponential, 125M params per node"),
+}
+
+
+def resolve(a, world):
+    """Fill the workload from --config (default 3 at N=1, 4 at N>1); explicit
+    flags override single fields.  Sets a.nodes (total) and a.scaling."""
+    if a.config is None:
+        a.config = 3 if world == 1 else 4
+    c = CONFIGS[a.config]
+    a.topology = a.topology or c["topology"]
+    a.algo = a.algo or c["algo"]
+    a.d = a.d or c["d"]
+    custom = any(getattr(a, k) != c[k] for k in ("topology", "algo", "d"))
+    if a.nodes_per_gpu:
+        a.nodes, a.scaling = a.nodes_per_gpu * world, "weak"
+    else:
+        a.nodes = a.nodes or c["nodes"]
+        a.scaling = "strong"
+    custom |= a.nodes != c["nodes"]
+    a.workload = (f"BASELINE {c['text']}" if not custom else
+                  f"custom (from BASELINE config {a.config}): {a.nodes} nodes, "
+                  f"{a.topology.replace('_', ' ')}, {a.d:,}-param bucket, {a.algo}")
+    return a
 
 
 def dist_env():
@@ -84,16 +129,15 @@ def algo_code(dg, algo):
 
 def config_block(a, world, nodes):
     return {
-        "workload": (f"BASELINE configs[1]/[4]: {a.topology.replace('_', ' ')} gossip, "
-                     f"{a.nodes_per_gpu} simulated nodes per B200 ({nodes} nodes), "
-                     f"{a.d:,}-param fp32 bucket per node, {a.algo}"),
-        "nodes": nodes, "nodes_per_gpu": a.nodes_per_gpu, "params_per_node": a.d,
+        "workload": a.workload, "baseline_config": a.config,
+        "nodes": nodes, "nodes_per_gpu": nodes / world, "params_per_node": a.d,
         "topology": a.topology, "algo": a.algo, "seed": SEED,
         "parallelism": (f"gossip over {world} GPU(s), nodes block-partitioned; remote buckets "
                         + ("read in-kernel from peer HBM over NVLink (CUDA IPC)" if a.transport == "p2p"
                            else "via chunked NCCL send/recv over NVLink")),
         "transport": a.transport,
-        "l2": "no flush needed: every step streams >= 28 GB per GPU, > 126 MB L2",
+        "l2": ("no flush needed: every step streams >= 28 GB per GPU, > 126 MB L2" if a.d * nodes >= 1 << 27
+               else "inputs smaller than L2: no flush (config 1 is a small-bucket, launch-bound case)"),
         "inputs": "synthetic StreamRng buckets (x0 ConsensusInit, g Minibatch@t=1 held fixed across timed steps)",
     }
 
@@ -157,7 +201,12 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def step_roofline(sched, world, d, steps_t, hbm_bw, transport, per_update=HBM_PER_UPDATE, algo="dadam"):
+def per_update_bytes(algo, t, s):
+    """DAdam 28 B; AccumAdam 28 B, 36 B on the fold step (t % s == 0)."""
+    return 36.0 if algo == "accum" and t % s == 0 else HBM_PER_UPDATE
+
+
+def step_roofline(sched, world, d, steps_t, hbm_bw, transport, algo="dadam", s=1):
     """SURVEY.md 8(d) per-GPU step bound, summed over the timed rounds:
     max over GPUs of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL).
     NCCL transport: every received remote bucket costs 12 B/param of HBM (owner
@@ -168,14 +217,15 @@ def step_roofline(sched, world, d, steps_t, hbm_bw, transport, per_update=HBM_PE
     n = sched.workers()
     if algo == "allreduce":  # column sums (8 B/elem written + read) + ring all-reduce of fp64 sums
         nl = -(-n // world)
-        t_hbm = d * (per_update * nl + 16.0) / hbm_bw
+        t_hbm = d * (HBM_PER_UPDATE * nl + 16.0) / hbm_bw
         t_nvl = (2.0 * (world - 1) / world) * 8.0 * d / NVL_MEASURED if world > 1 else 0.0
         return len(steps_t) * max(t_hbm, t_nvl)
     total = 0.0
     cache = {}
     for t in steps_t:
         r = (t - 1) % sched.period() + 1
-        if r not in cache:
+        per_update = per_update_bytes(algo, t, s)
+        if (r, per_update) not in cache:
             worst = 0.0
             for g in range(world):
                 sends, recvs = dg.plan_exchange(sched, world, g, r)
@@ -187,8 +237,8 @@ def step_roofline(sched, world, d, steps_t, hbm_bw, transport, per_update=HBM_PE
                 t_hbm = d * (per_update * nl + remote_hbm) / hbm_bw
                 t_nvl = 4.0 * d * max(len(recvs), len(sends)) / NVL_MEASURED
                 worst = max(worst, t_hbm, t_nvl)
-            cache[r] = worst
-        total += cache[r]
+            cache[(r, per_update)] = worst
+        total += cache[(r, per_update)]
     return total
 
 
@@ -262,7 +312,8 @@ def run_reference(a):
     rank, _, world = dist_env()
     if rank != 0:
         return
-    nodes = a.nodes_per_gpu * world
+    resolve(a, world)
+    nodes = a.nodes
     threads = os.cpu_count() or 1
     nodes_sample, d_sample = 8, 1 << 21
     rate, kind, note, el = cpu_reference_run(a, nodes_sample, d_sample, a.warmup + a.steps, threads)
@@ -270,7 +321,7 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": 1e3 * nodes_sample * d_sample / rate,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_block(a, world, nodes),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": min(threads, nodes_sample), "kind": kind,
                          "cpu_model": cpu_model(),
@@ -296,7 +347,8 @@ def run_ours(a):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    nodes = a.nodes_per_gpu * world
+    resolve(a, world)
+    nodes = a.nodes
     sched = make_schedule(dg, a.topology, nodes)
     algo = algo_code(dg, a.algo)
     h = hyper(a.algo)
@@ -371,7 +423,7 @@ def run_ours(a):
     achieved = st["timed_hbm_bytes"] / kern_s if kern_s > 0 else 0.0
     per_launch = st["timed_hbm_bytes"] / max(1, st["timed_launches"])
     transport = "p2p" if st["transport"] == dg.TRANSPORT_P2P else "nccl"
-    roof_step_s = step_roofline(sched, world, a.d, timed_t, hbm_bw, transport, algo=a.algo)
+    roof_step_s = step_roofline(sched, world, a.d, timed_t, hbm_bw, transport, algo=a.algo, s=h["s"])
 
     # ---- end to end through the public API: pinned host g -> H2D each step, step, D2H status
     e2e = None
@@ -407,16 +459,19 @@ def run_ours(a):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": a.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_block(a, world, nodes),
             "roofline": {"bound": "hbm", "achieved": achieved / 1e9, "peak": hbm_bw / 1e9, "unit": "GB/s",
                          "frac": achieved / hbm_bw, "traffic": read_traffic(key),
                          "algorithmic_bytes_per_launch": per_launch,
-                         "bytes_per_param_update": HBM_PER_UPDATE,
+                         "bytes_per_param_update": (HBM_PER_UPDATE if a.algo != "accum" else
+                                                    "28 (36 on fold steps t % s == 0)"),
                          "kernel_ms_per_launch": st["kernel_ms"] / max(1, st["timed_launches"]),
                          "kernel_share_of_step": st["kernel_ms"] / ms if ms > 0 else None,
                          "peak_source": peak_src,
-                         "kernel": "gossip_adam_fused (gossip_adam_warps for rounds of 4-8 single-node components)"},
+                         "kernel": ("gossip_adam_xshare<DEG,ALGO,FOLD,COLW> (csrc/xshare.cuh)"
+                                    if os.environ.get("DG_XSHARE", "1") != "0" else
+                                    "legacy.cu register-streaming kernels (DG_XSHARE=0)")},
             "step_roofline": {"bound_ms_per_step": 1e3 * roof_step_s / a.steps,
                               "frac": (roof_step_s * 1e3) / ms_max,
                               "model": ("SURVEY.md 8(d): per round, max over GPUs of max(HBM bytes/BW_HBM, "
@@ -437,6 +492,8 @@ def run_ours(a):
             "nccl_version": st["nccl_version"],
         }
         print(json.dumps(line), flush=True)
+    if dist:   # no peer may still read this rank's IPC-exported x when it is freed
+        dist.barrier()
     eng.close()
     if dist:
         dist.barrier()
