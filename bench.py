@@ -206,6 +206,54 @@ def per_update_bytes(algo, t, s):
     return 36.0 if algo == "accum" and t % s == 0 else HBM_PER_UPDATE
 
 
+class NvlCounters:
+    """NVLink data counters of this rank's GPU, read through NVML around the
+    timed region (hardware counters, not CUDA-event estimates).  Tries the
+    per-link data-throughput fields (KiB) first, then the per-link byte
+    counters; `read()` returns (tx_bytes, rx_bytes) summed over the links."""
+    LINKS = 18
+
+    def __init__(self, local):
+        self.h, self.src, self.err = None, None, None
+        try:
+            import pynvml
+            import torch
+            self.nv = pynvml
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(local).uuid)
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            for tx, rx, scale, name in (
+                    (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
+                     1024.0, "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX (KiB, per link)"),
+                    (pynvml.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, pynvml.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES,
+                     1.0, "NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES (per link)")):
+                self.ids, self.scale, self.src = (tx, rx), scale, name
+                try:
+                    if self.read() is not None:
+                        return
+                except Exception as e:  # noqa: BLE001
+                    self.err = f"{name}: {e}"
+            self.src = None
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+
+    def read(self):
+        if self.h is None or self.ids is None:
+            return None
+        q = [(fid, link) for fid in self.ids for link in range(self.LINKS)]
+        vals = self.nv.nvmlDeviceGetFieldValues(self.h, q)
+        out = [0.0, 0.0]
+        ok = False
+        for k, v in enumerate(vals):
+            if v.nvmlReturn != 0:
+                continue
+            ok = True
+            x = {0: v.value.dVal, 1: v.value.uiVal, 2: v.value.ulVal, 3: v.value.ullVal,
+                 4: v.value.sllVal, 5: v.value.siVal}.get(int(v.valueType), v.value.ullVal)
+            out[k // self.LINKS] += float(x) * self.scale
+        return tuple(out) if ok else None
+
+
 def step_roofline(sched, world, d, steps_t, hbm_bw, transport, algo="dadam", s=1):
     """SURVEY.md 8(d) per-GPU step bound, summed over the timed rounds:
     max over GPUs of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL).
@@ -396,8 +444,10 @@ def run_ours(a):
     eng.set_timing(False)
     eng.set_timing(True)
     launches0 = eng.stats()["kernel_launches"]
+    nvc = NvlCounters(local) if world > 1 else None
     barrier()
     torch.cuda.synchronize()
+    nv0 = nvc.read() if nvc else None
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(comp)
     timed_t = []
@@ -408,6 +458,7 @@ def run_ours(a):
     ev1.record(comp)
     eng.sync()
     torch.cuda.synchronize()
+    nv1 = nvc.read() if nvc else None
     barrier()
     ms = ev0.elapsed_time(ev1)
     st = eng.stats()
@@ -415,6 +466,30 @@ def run_ours(a):
     clk = clocks.stop() if rank == 0 else None
     ms_max = max_over_ranks(ms)
     launches = st["kernel_launches"] - launches0
+    nvl_counters = None
+    if nvc is not None:   # hardware NVLink counters of every rank, gathered to rank 0
+        mine = None
+        if nv0 is not None and nv1 is not None:
+            tx, rx = nv1[0] - nv0[0], nv1[1] - nv0[1]
+            mine = {"rank": rank, "tx_bytes_per_step": tx / a.steps, "rx_bytes_per_step": rx / a.steps,
+                    "rx_GBps_over_timed_region": rx / (ms / 1e3) / 1e9,
+                    "rx_GBps_over_exchange_kernels": (rx / (st["remote_kernel_ms"] / 1e3) / 1e9
+                                                      if st["remote_kernel_ms"] > 0 else None),
+                    "algorithmic_remote_bytes_per_step": st["remote_bytes"] / a.steps}
+        allc = [None] * world
+        dist.all_gather_object(allc, mine)
+        if all(c is not None for c in allc):
+            rxk = [c["rx_GBps_over_exchange_kernels"] for c in allc if c["rx_GBps_over_exchange_kernels"]]
+            nvl_counters = {"source": nvc.src, "per_rank": allc,
+                            "min_rx_GBps_over_exchange_kernels": min(rxk) if rxk else None,
+                            "peak": NVL_MEASURED / 1e9, "nominal": 900.0, "unit": "GB/s",
+                            "frac_of_measured": (min(rxk) * 1e9 / NVL_MEASURED) if rxk else None,
+                            "what": ("per GPU, NVLink data bytes received during the timed region (NVML "
+                                     "hardware counters read before/after it) over the summed CUDA-event "
+                                     "time of the exchange-round fused launches; counters include the "
+                                     "1-element barrier all-reduces")}
+        else:
+            nvl_counters = {"unavailable": nvc.err or "NVML NVLink counters not readable"}
     value = nodes * a.d * a.steps / (ms_max / 1e3)
 
     # ---- roofline of the dominant kernel (fused gossip+Adam), live CUDA events
@@ -487,6 +562,7 @@ def run_ours(a):
                                 "fused launches (per direction; every GPU both reads and serves)",
                         "peak_source": "measured peer read bandwidth, B200_PROFILING.md (775 GB/s LDG.128)"}
                        if st["remote_kernel_ms"] > 0 else None),
+            "nvlink_counters": nvl_counters,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
             "nvlink_bytes_sent_per_step": st["bytes_sent"] / max(1, st["steps"]),
             "nccl_version": st["nccl_version"],

@@ -316,6 +316,22 @@ struct dg_engine {
     const bool comm = !(p.send_node.empty() && p.recv_node.empty());
     return std::max(1, comm ? sm_total - reserve_sms : sm_total);
   }
+  // Fault injection for the exchange-protocol tests (DG_FAULT_*, read at
+  // create time; INTEGRATION.md "Environment"): delay this rank's streams,
+  // and overwrite every consumed buffer with NaN as soon as the protocol
+  // declares it free, so a missing wait shows up as a divergence or a
+  // mismatch instead of passing on benign timing.
+  long long fault_ns = 0;  // spin per step on this rank (DG_FAULT_DELAY_US, DG_FAULT_RANK)
+  bool poison = false;     // DG_FAULT_POISON=1
+  void fault_delay(cudaStream_t st) {
+    if (fault_ns > 0) {
+      dg::fault_spin<<<1, 1, 0, st>>>(fault_ns);
+      CU(cudaGetLastError());
+    }
+  }
+  void poison_range(float* p, size_t n, cudaStream_t st) {
+    if (poison && p && n) CU(cudaMemsetAsync(p, 0xFF, n * sizeof(float), st));  // 0xFFFFFFFF = NaN
+  }
   void enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
                      const dg::DevScalars& s, bool fold, long t, const float* const* slot_override = nullptr);
   void step(long t);
@@ -564,6 +580,7 @@ void dg_engine::step_range(long t, size_t off, size_t len) {
     nccl_register(rbuf, sizeof(float) * std::max(1, max_recv) * d_pad);
   }
   std::vector<const float*> slot_ptr(std::max<size_t>(1, p.recv_node.size()));
+  fault_delay(t & 1 ? comp : comm);
   if (comm_now) {
     auto it = range_posted.find(off);
     if (it == range_posted.end() || it->second != t) {  // not pre-posted: exchange x^(t-1) now
@@ -575,6 +592,8 @@ void dg_engine::step_range(long t, size_t off, size_t len) {
     for (size_t r = 0; r < p.recv_node.size(); ++r) slot_ptr[r] = rbuf + r * d_pad + off;
   }
   if (!diag_skip_kernel) enqueue_fused(p, off, len, 0, s, fold, t, comm_now ? slot_ptr.data() : nullptr);
+  if (comm_now)  // the range's recv buffers are consumed; the next exchange into them waits on comp
+    for (size_t r = 0; r < p.recv_node.size(); ++r) poison_range(rbuf + r * d_pad + off, len, comp);
   range_posted.erase(off);
   const dg::RoundPlan& q = plans[size_t(t % P)];
   if (G > 1 && !(q.send_node.empty() && q.recv_node.empty())) {
@@ -605,10 +624,14 @@ void dg_engine::step(long t) {
     // before the step after one (peers must have finished reading the buffer
     // this step may overwrite).  Every rank takes the same decision.
     const size_t prev = size_t((t - 2 + P) % P);
+    if (!(t & 1)) fault_delay(comp);  // late writer: peers wait for this rank at the barrier
     if (round_remote[ri] || (t > 1 && round_remote[prev])) {
       NC(ncclAllReduce(bar_buf, bar_buf, 1, ncclFloat, ncclSum, nccl, comp));
       ++barriers;
     }
+    if (t & 1) fault_delay(comp);  // late reader: this rank reads peers' x^(t-1) after they moved on
+    // no peer reads the stale x buffer past the barrier (it held x^(t-2) or older)
+    if (x_alt) poison_range(xcur ? arena[DG_BUF_X] : x_alt, NL * d_pad, comp);
     sent += 4.0 * double(d) * double(p.send_node.size());
     received += 4.0 * double(d) * double(p.recv_node.size());
     if (!p.pull) {
@@ -637,12 +660,17 @@ void dg_engine::step(long t) {
           CU(cudaStreamWaitEvent(comp, pull_ev[q], 0));
         }
         enqueue_fused(p, off, len, set, s, fold, t, slot_ptr);
+        poison_range(slots + size_t(set) * max_recv * chunk, size_t(max_recv) * chunk, comp);
         CU(cudaEventRecord(ev_slot_free[set], comp));
       }
     }
     if (p.pingpong) xcur ^= 1;
     return;
   }
+  fault_delay(t & 1 ? comp : comm);
+  // stale x buffer (x^(t-2) or older): its last readers -- step t-1's kernels and
+  // the sends they waited for -- are all ordered before this point on comp
+  if (x_alt) poison_range(xcur ? arena[DG_BUF_X] : x_alt, NL * d_pad, comp);
   if (p.send_node.empty() && p.recv_node.empty()) {  // intra-GPU round: one launch
     enqueue_fused(p, 0, d, 0, s, fold, t);
     if (p.pingpong) xcur ^= 1;
@@ -671,6 +699,7 @@ void dg_engine::step(long t) {
     // sends of the in-place x chunk have drained)
     CU(cudaStreamWaitEvent(comp, ev_recv[k], 0));
     if (!diag_skip_kernel) enqueue_fused(p, off, len, set, s, fold, t);
+    poison_range(slots + size_t(set) * max_recv * chunk, size_t(max_recv) * chunk, comp);
     CU(cudaEventRecord(ev_slot_free[set], comp));
   }
   if (p.pingpong) xcur ^= 1;
@@ -806,6 +835,9 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     e->sm_total = dg::sm_count(c->device);
     if (const char* rs = std::getenv("DG_RESERVE_SMS")) e->reserve_sms = std::max(0, std::atoi(rs));
     e->diag_skip_kernel = std::getenv("DG_DIAG_SKIP_KERNEL") != nullptr;
+    if (dg::env_int("DG_FAULT_RANK", e->G > 1 ? 1 : 0) == e->rank)
+      e->fault_ns = 1000LL * std::max(0, dg::env_int("DG_FAULT_DELAY_US", 0));
+    e->poison = dg::env_int("DG_FAULT_POISON", 0) != 0;
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU(cudaStreamCreateWithFlags(&e->comp, cudaStreamNonBlocking));

@@ -68,6 +68,8 @@ def test_every_engine_knob_is_documented():
     knobs = set()
     for f in glob.glob(os.path.join(root, "paper_2410_11998_b200", "csrc", "*.*")):
         if f.endswith((".cu", ".cuh", ".cpp", ".hpp")):
-            knobs |= set(re.findall(r'getenv\("([A-Z_0-9]+)"\)', open(f).read()))
+            src = open(f).read()
+            knobs |= set(re.findall(r'getenv\("([A-Z_0-9]+)"\)', src))
+            knobs |= set(re.findall(r'env_int\("([A-Z_0-9]+)"', src))
     doc = open(os.path.join(root, "INTEGRATION.md")).read()
     assert knobs and all(f"`{k}`" in doc for k in knobs), sorted(k for k in knobs if f"`{k}`" not in doc)

@@ -23,7 +23,12 @@ PATHS = {"default": {},                       # x-sharing kernel
          "tma_pingpong": {**LEGACY, "DG_TMA": "2", "DG_PINGPONG_MIN_NC": "1"},
          "per_thread_all": {**LEGACY, "DG_TMA": "0", "DG_COOP_MIN_NC": "99", "DG_PINGPONG_MIN_NC": "0"},
          "coop_all": {**LEGACY, "DG_TMA": "0", "DG_COOP_MIN_NC": "2", "DG_PINGPONG_MIN_NC": "0"},
-         "warps_all": {**LEGACY, "DG_TMA": "0", "DG_PINGPONG_MIN_NC": "1", "DG_WARPS_MIN_NC": "1"}}
+         "warps_all": {**LEGACY, "DG_TMA": "0", "DG_PINGPONG_MIN_NC": "1", "DG_WARPS_MIN_NC": "1"},
+         # fault injection (SPEC.md:317 Jacobi snapshot): a 2 ms spin before every
+         # step and the stale x buffer overwritten with NaN as soon as it is free
+         "fault_pingpong": {**LEGACY, "DG_PINGPONG_MIN_NC": "1", "DG_FAULT_POISON": "1",
+                            "DG_FAULT_DELAY_US": "2000"},
+         "fault_default": {"DG_FAULT_POISON": "1", "DG_FAULT_DELAY_US": "2000"}}
 
 
 @pytest.mark.parametrize("path", sorted(PATHS))

@@ -38,6 +38,36 @@ def test_multigpu_bit_exact(world, d, chunk, transport):
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
 
 
+FAULT = {"DG_FAULT_DELAY_US": "5000", "DG_FAULT_RANK": "1", "DG_FAULT_POISON": "1"}
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl", "p2p_pull_always", "p2p_direct_only"])
+def test_exchange_protocol_under_fault_injection(transport):
+    """SPEC.md:309/317/403: rank 1 runs 5 ms behind on every step (alternately
+    before the cross-GPU barrier -- a late writer -- and after it -- a late
+    reader), and every consumed buffer (stale x ping-pong buffer, NCCL recv
+    slots, pull slots) is overwritten with NaN the moment the protocol frees
+    it.  Results must stay bit-exact vs the oracle."""
+    world = min(4, torch.cuda.device_count())
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_parity_main.py")]
+    extra = {"p2p_pull_always": {"DG_P2P_PULL": "2"}, "p2p_direct_only": {"DG_P2P_PULL": "0"}}.get(transport, {})
+    env = {**os.environ, "MP_D": "100003", "MP_CHUNK": "16384", "MP_TRANSPORT": transport.split("_")[0],
+           **extra, **FAULT}
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+def test_ddp_multigpu_under_fault_injection():
+    """f1 bucketed exchange (step_range) with rank 1 delayed on alternate
+    streams and every consumed recv range poisoned with NaN."""
+    world = min(4, torch.cuda.device_count())
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_ddp_main.py")]
+    p = subprocess.run(cmd, env={**os.environ, **FAULT}, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+
+
 @pytest.mark.parametrize("transport", ["p2p"])
 def test_fullsize_configs_4_and_5(transport):
     """BASELINE config 4 (AER, 1.3B/node, AccumAdam s=4) on all visible GPUs (2 or 4) and
