@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--algo", choices=["dadam", "accum", "allreduce"], default=None)
     p.add_argument("--chunk", type=int, default=0)
     p.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
+    p.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                   help="replay the timed steps as one CUDA graph (dg_engine_run_steps); auto = on for "
+                        "buckets below 2^27 params per GPU (launch-bound, e.g. config 1)")
     p.add_argument("--e2e-steps", type=int, default=4)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -136,6 +139,7 @@ def config_block(a, world, nodes):
                         + ("read in-kernel from peer HBM over NVLink (CUDA IPC)" if a.transport == "p2p"
                            else "via chunked NCCL send/recv over NVLink")),
         "transport": a.transport,
+        "cuda_graph": bool(getattr(a, "use_graph", False)),
         "l2": ("no flush needed: every step streams >= 28 GB per GPU, > 126 MB L2" if a.d * nodes >= 1 << 27
                else "inputs smaller than L2: no flush (config 1 is a small-bucket, launch-bound case)"),
         "inputs": "synthetic StreamRng buckets (x0 ConsensusInit, g Minibatch@t=1 held fixed across timed steps)",
@@ -340,7 +344,7 @@ def cpu_model():
 def cpu_baseline(a, budget_s):
     import numpy as np  # noqa: F401
     threads = os.cpu_count() or 1
-    nodes_sample, d_sample = 8, 1 << 21
+    nodes_sample, d_sample = 8, min(a.d, 1 << 21)
     # calibrate: 2 steps, then size the run to ~budget_s
     rate, _, _, el = cpu_reference_run(a, nodes_sample, d_sample, 2, threads)
     steps = max(3, int(budget_s * rate / (nodes_sample * d_sample)))
@@ -363,7 +367,7 @@ def run_reference(a):
     resolve(a, world)
     nodes = a.nodes
     threads = os.cpu_count() or 1
-    nodes_sample, d_sample = 8, 1 << 21
+    nodes_sample, d_sample = 8, min(a.d, 1 << 21)
     rate, kind, note, el = cpu_reference_run(a, nodes_sample, d_sample, a.warmup + a.steps, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
@@ -430,10 +434,17 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    use_graph = a.use_graph = a.graph == "on" or (a.graph == "auto" and a.d * nodes // world < (1 << 27)
+                                    and a.algo != "allreduce")
     t = 0
-    for _ in range(a.warmup):
-        t += 1
-        eng.step(t)
+    if use_graph:   # warm-up range captured + replayed, the timed range captured (not run) here
+        eng.run_steps(1, a.warmup, graph=True)
+        t = a.warmup
+        eng.run_steps(t + 1, t + a.steps, graph=True, capture_only=True)
+    else:
+        for _ in range(a.warmup):
+            t += 1
+            eng.step(t)
     eng.sync()
 
     clocks = ClockSampler()
@@ -450,11 +461,14 @@ def run_ours(a):
     nv0 = nvc.read() if nvc else None
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(comp)
-    timed_t = []
-    for _ in range(a.steps):
-        t += 1
-        timed_t.append(t)
-        eng.step(t)
+    timed_t = list(range(t + 1, t + a.steps + 1))
+    if use_graph:
+        eng.run_steps(t + 1, t + a.steps, graph=True)
+        t += a.steps
+    else:
+        for _ in range(a.steps):
+            t += 1
+            eng.step(t)
     ev1.record(comp)
     eng.sync()
     torch.cuda.synchronize()

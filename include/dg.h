@@ -241,6 +241,14 @@ int dg_engine_consensus(dg_engine* e, double* dispersion, double* mean_sq);
 int dg_engine_consensus_fix_mean(dg_engine* e);
 /* One fused gossip + Adam step for iteration t (>= 1); asynchronous. */
 int dg_engine_step(dg_engine* e, long t);
+/* Steps t_first..t_last in order (the trainsim hot loop).
+ * flags & DG_RUN_GRAPH: the range is captured once into a CUDA graph (cached
+ * per (t_first, t_last) and starting x buffer) and replayed as one graph
+ * launch -- for small buckets whose steps are launch-bound (BASELINE config
+ * 1); DG_RUN_CAPTURE_ONLY: capture (no execution) so a later call replays.
+ * Results are identical to calling dg_engine_step for each t. */
+enum { DG_RUN_GRAPH = 1, DG_RUN_CAPTURE_ONLY = 2 };
+int dg_engine_run_steps(dg_engine* e, long t_first, long t_last, int flags);
 /* Bucketed step (the paper's per-bucket update U_k, PAPER.md:302-304 and
  * 1089-1095).  Updates elements [off, off+len) of every
  * resident node for iteration t -- mixing with round-t peers, Adam -- after

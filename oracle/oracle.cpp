@@ -799,6 +799,12 @@ int or_step_all_f64(const or_sched* s, int algo, const or_adam_cfg* cfg, size_t 
   set_threads(threads);
   return step_all<double>(s, algo, cfg, d, t, T, 0, false, g, x, xprev, m, v, b);
 }
+int or_step_all_f32(const or_sched* s, int algo, const or_adam_cfg* cfg, size_t d, long t, long T,
+                    int threads, const float* g, float* x, float* xprev, float* m, float* v, float* b) {
+  if (!s) return fail(OR_CONFIG_ERROR, "step_all: empty schedule");
+  set_threads(threads);
+  return step_all<float>(s, algo, cfg, d, t, T, 0, false, g, x, xprev, m, v, b);
+}
 int or_run_cols_f32(const or_sched* s, int algo, const or_adam_cfg* cfg, uint64_t seed,
                     const uint64_t* cols, size_t nc, int dispersed, long t0, long t1, long T,
                     int threads, float* x, float* m, float* v, float* b) {

@@ -105,6 +105,11 @@ int or_run_f32(const or_sched* s, int algo, const or_adam_cfg* cfg, uint64_t see
 int or_step_all_f64(const or_sched* s, int algo, const or_adam_cfg* cfg, size_t d, long t,
                     long T, int threads, const double* g, double* x, double* x_prev, double* m,
                     double* v, double* b);
+/* fp32 mirror of one step with a caller-supplied gradient (e.g. g held fixed
+ * across steps, as the CUDA-graph step ranges of the engine replay it). */
+int or_step_all_f32(const or_sched* s, int algo, const or_adam_cfg* cfg, size_t d, long t,
+                    long T, int threads, const float* g, float* x, float* x_prev, float* m,
+                    float* v, float* b);
 int or_max_threads(void);
 
 /* Column-sampled run: every parameter column evolves independently of the

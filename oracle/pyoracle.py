@@ -93,6 +93,8 @@ def lib():
                                                         C.c_int, p, p, p, C.c_void_p]
         L.or_step_all_f64.argtypes = [C.c_void_p, C.c_int, C.POINTER(AdamCfg), C.c_size_t, C.c_long,
                                       C.c_long, C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_void_p]
+        L.or_step_all_f32.argtypes = [C.c_void_p, C.c_int, C.POINTER(AdamCfg), C.c_size_t, C.c_long,
+                                      C.c_long, C.c_int, _fp, _fp, _fp, _fp, _fp, C.c_void_p]
         _lib = L
     return _lib
 
@@ -315,6 +317,21 @@ def run(s, algo, cfg, seed, state, t_begin, t_end, T=0, threads=0):
     c = cfg.c()
     _check(fn(s.handle, algo, C.byref(c), seed, d, t_begin, t_end, T, threads,
               x.reshape(-1), state["m"].reshape(-1), state["v"].reshape(-1), _ptr(state["b"])))
+    return state
+
+
+def run_fixed_g(s, algo, cfg, state, g, t_begin, t_end, T=0, threads=0):
+    """fp32 mirror (or fp64) steps t_begin..t_end with the gradient g (n x d) held fixed."""
+    x = state["x"]
+    n, d = x.shape
+    xprev = np.empty_like(x)
+    f64 = x.dtype == np.float64
+    fn = lib().or_step_all_f64 if f64 else lib().or_step_all_f32
+    g = np.ascontiguousarray(g, x.dtype)
+    c = cfg.c()
+    for t in range(t_begin, t_end + 1):
+        _check(fn(s.handle, algo, C.byref(c), d, t, T, threads, g.reshape(-1), x.reshape(-1), xprev.reshape(-1),
+                  state["m"].reshape(-1), state["v"].reshape(-1), _ptr(state["b"])))
     return state
 
 

@@ -39,6 +39,7 @@ _LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg.so")
 DADAM, ACCUM, ALLREDUCE = 0, 1, 2
 TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_P2P = 0, 1, 2
 ENGINE_IN_PLACE = 1
+RUN_GRAPH, RUN_CAPTURE_ONLY = 1, 2
 X, G, M, V, ACC = 0, 1, 2, 3, 4
 
 
@@ -157,6 +158,7 @@ SIGNATURES = {
     "dg_engine_consensus": ([_VP, _DP, _DP], _I),
     "dg_engine_consensus_fix_mean": ([_VP], _I),
     "dg_engine_step": ([_VP, _L], _I),
+    "dg_engine_run_steps": ([_VP, _L, _L, _I], _I),
     "dg_engine_sync": ([_VP], _I),
     "dg_engine_streams": ([_VP, C.POINTER(_VP), C.POINTER(_VP)], _I),
     "dg_engine_get_stats": ([_VP, C.POINTER(_EngineStats)], _I),
@@ -569,6 +571,12 @@ class Engine:
 
     def step(self, t: int):
         _check(lib().dg_engine_step(self._h, t))
+
+    def run_steps(self, t_first: int, t_last: int, graph: bool = True, capture_only: bool = False):
+        """Steps t_first..t_last; graph=True replays them as one cached CUDA graph
+        (dg_engine_run_steps), identical results to calling step(t) for each t."""
+        flags = (RUN_GRAPH if graph else 0) | (RUN_CAPTURE_ONLY if capture_only else 0)
+        _check(lib().dg_engine_run_steps(self._h, t_first, t_last, flags))
 
     def step_range(self, t: int, off: int, length: int):
         _check(lib().dg_engine_step_range(self._h, t, off, length))

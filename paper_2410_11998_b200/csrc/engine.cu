@@ -335,6 +335,25 @@ struct dg_engine {
   void enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
                      const dg::DevScalars& s, bool fold, long t, const float* const* slot_override = nullptr);
   void step(long t);
+  // CUDA graphs of whole step ranges (dg_engine_run_steps): small buckets are
+  // launch-bound (BASELINE config 1: 8 x 2^20 params, ~36 us of HBM per step),
+  // so t_first..t_last are captured once from the compute stream (and the
+  // streams it forks to) and replayed as one graph launch.  A graph bakes in
+  // the x buffer it starts from, so it replays only from the same xcur.
+  struct GraphRec {
+    long t0 = 0, t1 = 0;
+    int x0 = 0, x1 = 0;
+    cudaGraphExec_t exec = nullptr;
+    long launches = 0, steps = 0, barriers = 0;
+    double hbm = 0, sent = 0, received = 0, remote = 0;
+  };
+  std::vector<GraphRec> graphs;
+  bool capturing = false;
+  double cap_hbm = 0, cap_remote = 0;
+  long cap_launches = 0;
+  std::vector<long> tev_n;  // kernels covered by each timed record
+  GraphRec& capture(long t0, long t1);
+  void run_steps(long t0, long t1, int flags);
   ~dg_engine();
 };
 
@@ -375,6 +394,8 @@ dg_engine::~dg_engine() {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
   }
+  for (auto& gr : graphs)
+    if (gr.exec) cudaGraphExecDestroy(gr.exec);
   if (comp) cudaStreamDestroy(comp);
   if (comm) cudaStreamDestroy(comm);
   for (auto st : pull) cudaStreamDestroy(st);
@@ -490,6 +511,16 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
 
 template <class F>
 void dg_engine::timed(double bytes, double nvl_bytes, F&& launch) {
+  if (capturing) {  // recorded into a graph: no per-launch events, bytes kept for the replays
+    launch();
+    dg::cuda_check(cudaGetLastError(), "kernel launch (capture)");
+    ++cap_launches;
+    cap_hbm += bytes;
+    cap_remote += nvl_bytes;
+    ++launches;
+    hbm += bytes;
+    return;
+  }
   if (timing) {
     if (tev_used == tev.size()) {
       cudaEvent_t a, b;
@@ -498,6 +529,7 @@ void dg_engine::timed(double bytes, double nvl_bytes, F&& launch) {
       tev.push_back({a, b});
       tev_bytes.push_back(0);
       tev_remote.push_back(0);
+      tev_n.push_back(1);
     }
     CU(cudaEventRecord(tev[tev_used].first, comp));
   }
@@ -506,6 +538,7 @@ void dg_engine::timed(double bytes, double nvl_bytes, F&& launch) {
   if (timing) {
     CU(cudaEventRecord(tev[tev_used].second, comp));
     tev_remote[tev_used] = nvl_bytes;
+    tev_n[tev_used] = 1;
     tev_bytes[tev_used++] = bytes;
   }
   ++launches;
@@ -540,7 +573,7 @@ void dg_engine::harvest_timing() {
     CU(cudaEventElapsedTime(&ms, tev[k].first, tev[k].second));
     kernel_ms += ms;
     timed_bytes += tev_bytes[k];
-    ++timed_launches;
+    timed_launches += tev_n[k];
     if (tev_remote[k] > 0) {
       remote_ms += ms;
       remote_bytes += tev_remote[k];
@@ -703,6 +736,85 @@ void dg_engine::step(long t) {
     CU(cudaEventRecord(ev_slot_free[set], comp));
   }
   if (p.pingpong) xcur ^= 1;
+}
+
+dg_engine::GraphRec& dg_engine::capture(long t0, long t1) {
+  for (auto& gr : graphs)
+    if (gr.t0 == t0 && gr.t1 == t1 && gr.x0 == xcur) return gr;
+  if (graphs.size() >= 8) {  // small cache: oldest out
+    CU(cudaGraphExecDestroy(graphs.front().exec));
+    graphs.erase(graphs.begin());
+  }
+  GraphRec gr;
+  gr.t0 = t0;
+  gr.t1 = t1;
+  gr.x0 = xcur;
+  // host-side bookkeeping that step() advances while capturing; restored
+  // after, and re-applied on every replay
+  const long l0 = launches, s0 = steps, b0 = barriers;
+  const double h0 = hbm, se0 = sent, r0 = received;
+  cap_hbm = cap_remote = 0;
+  cap_launches = 0;
+  cudaGraph_t g = nullptr;
+  CU(cudaStreamBeginCapture(comp, cudaStreamCaptureModeThreadLocal));
+  capturing = true;
+  try {
+    for (long t = t0; t <= t1; ++t) step(t);
+  } catch (...) {
+    capturing = false;
+    cudaStreamEndCapture(comp, &g);
+    if (g) cudaGraphDestroy(g);
+    xcur = gr.x0;
+    launches = l0, steps = s0, barriers = b0, hbm = h0, sent = se0, received = r0;
+    throw;
+  }
+  capturing = false;
+  CU(cudaStreamEndCapture(comp, &g));
+  gr.x1 = xcur;
+  xcur = gr.x0;
+  gr.launches = launches - l0, gr.steps = steps - s0, gr.barriers = barriers - b0;
+  gr.hbm = hbm - h0, gr.sent = sent - se0, gr.received = received - r0, gr.remote = cap_remote;
+  launches = l0, steps = s0, barriers = b0, hbm = h0, sent = se0, received = r0;
+  const cudaError_t ie = cudaGraphInstantiate(&gr.exec, g, 0);
+  cudaGraphDestroy(g);
+  CU(ie);
+  graphs.push_back(gr);
+  return graphs.back();
+}
+
+void dg_engine::run_steps(long t0, long t1, int flags) {
+  if (t0 < 1 || t1 < t0) dg::config_error("run_steps: need 1 <= t_first <= t_last");
+  if (!range_posted.empty())
+    dg::config_error("run_steps: bucketed exchanges are in flight (use dg_engine_step_range consistently)");
+  CU(cudaSetDevice(device));
+  if (!(flags & DG_RUN_GRAPH)) {
+    for (long t = t0; t <= t1; ++t) step(t);
+    return;
+  }
+  GraphRec& gr = capture(t0, t1);
+  if (flags & DG_RUN_CAPTURE_ONLY) return;
+  if (timing) {
+    if (tev_used == tev.size()) {
+      cudaEvent_t a, b;
+      CU(cudaEventCreate(&a));
+      CU(cudaEventCreate(&b));
+      tev.push_back({a, b});
+      tev_bytes.push_back(0);
+      tev_remote.push_back(0);
+      tev_n.push_back(1);
+    }
+    CU(cudaEventRecord(tev[tev_used].first, comp));
+  }
+  CU(cudaGraphLaunch(gr.exec, comp));
+  if (timing) {
+    CU(cudaEventRecord(tev[tev_used].second, comp));
+    tev_bytes[tev_used] = gr.hbm;
+    tev_remote[tev_used] = gr.remote;
+    tev_n[tev_used++] = gr.launches;
+  }
+  xcur = gr.x1;
+  launches += gr.launches, steps += gr.steps, barriers += gr.barriers;
+  hbm += gr.hbm, sent += gr.sent, received += gr.received;
 }
 
 // ===================================================================== C ABI
@@ -1113,6 +1225,13 @@ int dg_engine_step(dg_engine* e, long t) {
   return guarded([&] {
     if (!e) dg::config_error("engine_step: null handle");
     e->step(t);
+  });
+}
+
+int dg_engine_run_steps(dg_engine* e, long t_first, long t_last, int flags) {
+  return guarded([&] {
+    if (!e) dg::config_error("engine_run_steps: null handle");
+    e->run_steps(t_first, t_last, flags);
   });
 }
 

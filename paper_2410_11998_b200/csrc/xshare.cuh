@@ -23,10 +23,12 @@
 // however many members mix it; the round-1 warp-per-node kernel converted it
 // once per reader (6x for static exponential), which kept its XU pipe ~45 %
 // busy at the HBM roofline.  Here a thread holds one member's 4-5 float4
-// streams: 3 CTAs of 8 warps per SM.  Lane 0 of every warp bulk-prefetches
-// its streams (cp.async.bulk.prefetch.L2) DG_PREFETCH column blocks ahead,
-// so the demand loads mostly hit L2: the DRAM latency is covered without
-// registers.
+// streams: 3 CTAs of 8 warps per SM.  Every lane prefetches its streams into
+// L2 (prefetch.global.L2) DG_PREFETCH column blocks ahead, so the demand loads
+// mostly hit L2, and the x^(t-1) row is loaded one column block ahead (4
+// registers), so the conversion never waits on DRAM: the latency is covered
+// without holding a second copy of g, m, v in registers.  Non-finite results
+// are detected by an FFMA-by-zero accumulator (nan_acc), one vote per launch.
 //
 // Jacobi snapshot: every read of a column's x rows (step 1)
 // precedes the barrier, every x^(t) store of that column (step 3) follows it,
@@ -78,6 +80,19 @@ constexpr int kShBufD2 = (kShRows + 1) * kShRowD2;  // double2 per buffer
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+#ifndef DG_XS_PF
+#define DG_XS_PF 1      // per-lane prefetch.global.L2 (0: lane-0 bulk prefetch)
+#endif
+#ifndef DG_XS_NANACC
+#define DG_XS_NANACC 1  // non-finite detection by FFMA-by-zero accumulation (0: isfinite)
+#endif
+#ifndef DG_XS_XPIPE
+#define DG_XS_XPIPE 1   // x^(t-1) rows loaded one column block ahead (0: just in time)
+#endif
 
 #ifndef DG_XS_MINB
 #define DG_XS_MINB 3  // resident CTAs per SM the register budget is sized for
@@ -127,10 +142,27 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
     const int b = threadIdx.x / kShRowD2, i = threadIdx.x % kShRowD2;
     P[b * kShBufD2 + kShRows * kShRowD2 + i] = make_double2(0.0, 0.0);
   }
-  // lane 0: bulk L2 prefetch of this warp's streams for column block blk
+  // L2 prefetch of this warp's streams DG_PREFETCH column blocks ahead.
+  // DG_XS_PF=1 (default): every lane prefetches its own 16 B with
+  // prefetch.global.L2 (one warp instruction per stream, 4 lines).
+  // DG_XS_PF=0: lane 0 issues one cp.async.bulk.prefetch.L2 per stream (the
+  // operand must be uniform, so the compiler wraps each in a waterfall loop:
+  // ~90 instructions per column block, measured).
   const int pd = a.prefetch;
   auto prefetch = [&](long long i) {
-    if (lane != 0 || i >= count) return;
+    if (i >= count) return;
+#if DG_XS_PF
+    const long long pe = (((first + i * step) << 5) + lane) << 2;
+    if (pe >= a.n) return;
+    if (member) {
+      prefetch_l2_line(gq + pe);
+      prefetch_l2_line(mq + pe);
+      prefetch_l2_line(vq + pe);
+      if (ALGO == 1) prefetch_l2_line(bq + pe);
+    }
+    if (pf_x) prefetch_l2_line(xr + pe);
+#else
+    if (lane != 0) return;
     const long long e = (first + i * step) << 7;  // first element of the block
     const uint32_t bytes = uint32_t(min(128LL, ((a.n - e) + 3) & ~3LL)) * 4u;
     if (member) {
@@ -140,10 +172,24 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
       if (ALGO == 1) prefetch_l2(bq + e, bytes);
     }
     if (pf_x) prefetch_l2(xr + e, bytes);
+#endif
   };
   for (int i = 0; i < pd; ++i) prefetch(i);
+#if DG_XS_NANACC
+  float z = 0.0f;  // non-finite accumulator (nan_acc)
+#endif
   bool bad = false;
   int buf = 0;
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#if DG_XS_XPIPE
+  // x^(t-1) row loaded one column block ahead: the conversion below never
+  // waits on DRAM, so the warps reach the barrier together
+  float4 xnext = zero4;
+  if (conv && count > 0) {
+    const long long q0 = (first << 5) + lane;
+    if (q0 < n4) xnext = ld4(xr + (q0 << 2));
+  }
+#endif
   for (long long i = 0; i < count; ++i, buf ^= 1) {
     prefetch(i + pd);
     const long long q = ((first + i * step) << 5) + lane;
@@ -158,7 +204,15 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
     }
     double2* Pb = P + buf * kShBufD2;
     if (conv) {
-      const float4 x = live ? ld4(xr + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+#if DG_XS_XPIPE
+      const float4 x = xnext;
+      if (i + 1 < count) {
+        const long long q1 = ((first + (i + 1) * step) << 5) + lane;
+        xnext = q1 < n4 ? ld4(xr + (q1 << 2)) : zero4;
+      }
+#else
+      const float4 x = live ? ld4(xr + e) : zero4;
+#endif
       double2 lo, hi;
       if (COLW) {
         lo = make_double2(__dmul_rn(wr, double(x.x)), __dmul_rn(wr, double(x.y)));
@@ -192,20 +246,42 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
                                     __double2float_rn(aw));
       float4 x;
       if (ALGO == 0) {
+#if DG_XS_NANACC
+        dadam_core(mx.x, g.x, x.x, m.x, v.x, a.s);
+        dadam_core(mx.y, g.y, x.y, m.y, v.y, a.s);
+        dadam_core(mx.z, g.z, x.z, m.z, v.z, a.s);
+        dadam_core(mx.w, g.w, x.w, m.w, v.w, a.s);
+        nan_acc(z, x.x, m.x, v.x);
+        nan_acc(z, x.y, m.y, v.y);
+        nan_acc(z, x.z, m.z, v.z);
+        nan_acc(z, x.w, m.w, v.w);
+#else
         bool ok = dadam_elem(mx.x, g.x, x.x, m.x, v.x, a.s);
         ok &= dadam_elem(mx.y, g.y, x.y, m.y, v.y, a.s);
         ok &= dadam_elem(mx.z, g.z, x.z, m.z, v.z, a.s);
         ok &= dadam_elem(mx.w, g.w, x.w, m.w, v.w, a.s);
         bad |= !ok;
+#endif
         st4(xq + e, x);
         st4_mv(mq + e, m);
         st4_mv(vq + e, v);
       } else {
+#if DG_XS_NANACC
+        accum_core<FOLD>(mx.x, g.x, x.x, m.x, v.x, bb.x, a.s);
+        accum_core<FOLD>(mx.y, g.y, x.y, m.y, v.y, bb.y, a.s);
+        accum_core<FOLD>(mx.z, g.z, x.z, m.z, v.z, bb.z, a.s);
+        accum_core<FOLD>(mx.w, g.w, x.w, m.w, v.w, bb.w, a.s);
+        nan_acc(z, x.x, m.x, v.x);
+        nan_acc(z, x.y, m.y, v.y);
+        nan_acc(z, x.z, m.z, v.z);
+        nan_acc(z, x.w, m.w, v.w);
+#else
         bool ok = accum_elem<FOLD>(mx.x, g.x, x.x, m.x, v.x, bb.x, a.s);
         ok &= accum_elem<FOLD>(mx.y, g.y, x.y, m.y, v.y, bb.y, a.s);
         ok &= accum_elem<FOLD>(mx.z, g.z, x.z, m.z, v.z, bb.z, a.s);
         ok &= accum_elem<FOLD>(mx.w, g.w, x.w, m.w, v.w, bb.w, a.s);
         bad |= !ok;
+#endif
         st4(xq + e, x);
         st4_mv(bq + e, bb);
         if (FOLD) {
@@ -215,6 +291,9 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
       }
     }
   }
+#if DG_XS_NANACC
+  bad = z != z;
+#endif
   // scalar tail (n % 4 elements): CTA 0, lane l of member warp w takes element
   // n4*4 + l; all x reads precede the barrier, all writes follow it
   const long long tail0 = n4 << 2;
