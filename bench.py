@@ -225,7 +225,8 @@ class NvlCounters:
             self.nv = pynvml
             pynvml.nvmlInit()
             uuid = str(torch.cuda.get_device_properties(local).uuid)
-            self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            self.uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(self.uuid)
             for tx, rx, scale, name in (
                     (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
                      1024.0, "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX (KiB, per link)"),
@@ -237,25 +238,53 @@ class NvlCounters:
                         return
                 except Exception as e:  # noqa: BLE001
                     self.err = f"{name}: {e}"
-            self.src = None
+            errs = self.err
+            self.src = "nvidia-smi"
+            if self.read() is None:
+                self.src = None
+                self.err = f"{errs}; {self.err}"
         except Exception as e:  # noqa: BLE001
             self.err = str(e)
 
     def read(self):
+        if self.src == "nvidia-smi":
+            return self._read_smi()
         if self.h is None or self.ids is None:
             return None
         q = [(fid, link) for fid in self.ids for link in range(self.LINKS)]
         vals = self.nv.nvmlDeviceGetFieldValues(self.h, q)
         out = [0.0, 0.0]
         ok = False
+        codes = set()
         for k, v in enumerate(vals):
             if v.nvmlReturn != 0:
+                codes.add(int(v.nvmlReturn))
                 continue
             ok = True
             x = {0: v.value.dVal, 1: v.value.uiVal, 2: v.value.ulVal, 3: v.value.ullVal,
                  4: v.value.sllVal, 5: v.value.siVal}.get(int(v.valueType), v.value.ullVal)
             out[k // self.LINKS] += float(x) * self.scale
+        if not ok:
+            self.err = f"{self.src}: nvmlReturn codes {sorted(codes)}"
         return tuple(out) if ok else None
+
+    def _read_smi(self):
+        """`nvidia-smi nvlink -gt d`: per-link Data Tx / Rx counters in KiB."""
+        import re
+        p = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", self.uuid], capture_output=True, text=True,
+                           timeout=30)
+        tx = rx = 0.0
+        hits = 0
+        for m in re.finditer(r"Data\s+(Tx|Rx)\s*:\s*([0-9]+)\s*KiB", p.stdout):
+            hits += 1
+            if m.group(1) == "Tx":
+                tx += float(m.group(2)) * 1024.0
+            else:
+                rx += float(m.group(2)) * 1024.0
+        if not hits:
+            self.err = (self.err or "") + f"; nvidia-smi nvlink -gt d: {p.stdout[:200]!r} {p.stderr[:200]!r}"
+            return None
+        return tx, rx
 
 
 def step_roofline(sched, world, d, steps_t, hbm_bw, transport, algo="dadam", s=1):

@@ -105,6 +105,8 @@ struct RoundPlan {
   // >= 1.75x on average: in-kernel peer loads bypass the local L2 and cross
   // NVLink once per reader, but run ~1.8x faster than copy-engine pulls)
   bool pull = false;
+  // run on the x-sharing kernel (xshare.cuh); otherwise the legacy.cu kernels
+  bool xshare = false;
   // exchange (ordered by (peer, node))
   std::vector<int> send_peer, send_node;  // send_node: global id of a resident node
   std::vector<int> recv_peer, recv_node;  // recv slot r holds recv_node[r]

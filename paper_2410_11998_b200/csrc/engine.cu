@@ -5,6 +5,7 @@
 // Replaces the hot loop of the reference's trainsim (Jacobi
 // snapshot, mixed sum, per-worker dadam_step / accum_adam_step) and the
 // paper's bucketed overlap (Fig. 1).
+#include <cuda.h>  // CUstream / CUdeviceptr types for the stream memory operations (entry points)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -105,6 +106,49 @@ int* semantic_flag() {
   void* p = nullptr;
   CU(cudaGetSymbolAddress(&p, g_semantic_flag));
   return static_cast<int*>(p);
+}
+
+// ------------------------------------------------------------------ stream memory operations
+// In-place P2P transport (DDP buckets): per-range cross-GPU ordering with
+// stream-ordered 64-bit flags -- cuStreamWaitValue64 on this GPU's own flag
+// array (the front end waits, no SM spins) and cuStreamWriteValue64 into the
+// peers' flag arrays (IPC-mapped), resolved through the runtime's driver
+// entry points so libdg does not link libcuda.
+struct MemOps {
+  CUresult (*wait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+  CUresult (*write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+};
+const MemOps& memops() {
+  static const MemOps m = [] {
+    MemOps r;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", reinterpret_cast<void**>(&r.wait64), cudaEnableDefault,
+                                &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      r.wait64 = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", reinterpret_cast<void**>(&r.write64), cudaEnableDefault,
+                                &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      r.write64 = nullptr;
+    cudaGetLastError();
+    return r;
+  }();
+  return m;
+}
+void cu_check(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) throw Error(DG_CUDA_ERROR, std::string(what) + ": CUresult " + std::to_string(int(r)));
+}
+// DG_SIGNAL_KERNEL=1: peers' flags written by a 1-warp kernel (release stores
+// over NVLink) instead of cuStreamWriteValue64
+constexpr int kMaxSignal = 8;
+struct SignalArgs {
+  unsigned long long* dst[kMaxSignal];
+  int n;
+  unsigned long long value;
+};
+__global__ void signal_peers(const __grid_constant__ SignalArgs a) {
+  if (threadIdx.x < a.n) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.dst[threadIdx.x]), "l"(a.value) : "memory");
+  }
 }
 
 // ------------------------------------------------------------------ x-sharing launch (default K1)
@@ -251,7 +295,8 @@ struct dg_engine {
   dg::ShArgs sargs;
   void launch_groups(const dg::GroupPlan& tp, float* const* x, float* const* xo, const float* const* g,
                           float* const* m, float* const* v, float* const* b, const float* const* slot_ptr,
-                          size_t off, size_t len, const dg::DevScalars& s, bool fold, long t, int sms);
+                          size_t off, size_t len, const dg::DevScalars& s, bool fold, long t, int sms,
+                          float* const* xp = nullptr);
   // optional per-launch CUDA-event timing (bench roofline)
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
@@ -333,8 +378,26 @@ struct dg_engine {
     if (poison && p && n) CU(cudaMemsetAsync(p, 0xFF, n * sizeof(float), st));  // 0xFFFFFFFF = NaN
   }
   void enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
-                     const dg::DevScalars& s, bool fold, long t, const float* const* slot_override = nullptr);
+                     const dg::DevScalars& s, bool fold, long t, const float* const* slot_override = nullptr,
+                     float* const* xpub_out = nullptr);
   void step(long t);
+  // In-place P2P transport (DG_ENGINE_IN_PLACE + P2P; the f1 DDP wrapper):
+  // x never moves, so each update also publishes x^(t) into xpub[t % 2],
+  // which peers read in-kernel over NVLink at t + 1.  Per range and rank, a
+  // 64-bit flag "finished iteration v - 1" orders it: before updating range
+  // k at t a rank waits until every peer signalled t (its x^(t-1) is
+  // published and it has finished reading our x^(t-2) in xpub[t % 2]), then
+  // signals t + 1 to every peer.
+  bool inplace_p2p = false;
+  float* xpub[2] = {};                      // [NL][d_pad] each
+  unsigned long long* sig = nullptr;        // [kMaxRanges][G], written by the peers
+  std::vector<unsigned long long*> peer_sig;  // every rank's sig (own = sig)
+  std::map<size_t, int> range_slot;         // range offset -> flag row (first-use order)
+  std::map<size_t, long> range_last;        // last iteration stepped per range
+  bool signal_kernel = false;
+  static constexpr int kMaxRanges = 4096;
+  void step_range_p2p(long t, size_t off, size_t len);
+  void signal_range(int slot, unsigned long long value);
   // CUDA graphs of whole step ranges (dg_engine_run_steps): small buckets are
   // launch-bound (BASELINE config 1: 8 x 2^20 params, ~36 us of HBM per step),
   // so t_first..t_last are captured once from the compute stream (and the
@@ -375,6 +438,11 @@ dg_engine::~dg_engine() {
   if (slots) cudaFree(slots);
   if (x_alt) cudaFree(x_alt);
   if (bar_buf) cudaFree(bar_buf);
+  for (int r = 0; r < int(peer_sig.size()); ++r)
+    if (r != rank && peer_sig[r]) cudaIpcCloseMemHandle(peer_sig[r]);
+  for (float* p : xpub)
+    if (p) cudaFree(p);
+  if (sig) cudaFree(sig);
   for (int b = 0; b < 2; ++b)
     for (int r = 0; r < int(peer_base[b].size()); ++r)
       if (r != rank && peer_base[b][r]) cudaIpcCloseMemHandle(peer_base[b][r]);
@@ -403,7 +471,8 @@ dg_engine::~dg_engine() {
 }
 
 void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, int slot_set,
-                              const dg::DevScalars& s, bool fold, long t, const float* const* slot_override) {
+                              const dg::DevScalars& s, bool fold, long t, const float* const* slot_override,
+                              float* const* xpub_out) {
   float *x[dg::kMaxLocal], *xo[dg::kMaxLocal], *m[dg::kMaxLocal], *v[dg::kMaxLocal], *b[dg::kMaxLocal];
   const float* g[dg::kMaxLocal];
   for (int i = 0; i < NL; ++i) {
@@ -420,13 +489,13 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
                   : transport == DG_TRANSPORT_P2P ? peer_x(p.recv_node[r]) + off
                                                   : slots + (size_t(slot_set) * max_recv + r) * chunk;
   const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr};
-  const bool st_k = xshare;
+  const bool st_k = p.xshare;
   const bool tma = !st_k && dg::use_tma(p);
   dg::LaunchFn fn = nullptr;
   const dg::GroupPlan* tp = nullptr;
   if (st_k) {
     const size_t ri = size_t(&p - plans.data());
-    if (ri >= gplans.size()) throw dg::Error(DG_INVARIANT, "xshare: plan not owned by the engine");
+    if (ri >= gplans.size() || !gplans[ri].ok) throw dg::Error(DG_INVARIANT, "xshare: plan not owned by the engine");
     tp = &gplans[ri];
   } else if (!tma) {
     dg::fill_args(argbuf, p, bf, off, len, s, int(t), flag);
@@ -435,16 +504,18 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   // algorithmic LOCAL HBM bytes of this launch (remote buckets: recv-slot reads
   // for NCCL; for P2P they come over NVLink and are counted in `received`)
   const double per = algo == DG_ALGO_DADAM ? 28.0 : (fold ? 36.0 : 28.0);
-  const double remote_hbm =
-      (transport == DG_TRANSPORT_P2P && !slot_override) ? 0.0 : 4.0 * double(p.recv_node.size());
-  const double bytes = double(len) * (per * p.n_local + remote_hbm);
-  // NVLink bytes the launch reads in-kernel (P2P exchange rounds)
-  const double nvl = (transport == DG_TRANSPORT_P2P && !slot_override)
+  const double remote_hbm = ((transport == DG_TRANSPORT_P2P && !slot_override) || xpub_out)
+                                ? 0.0
+                                : 4.0 * double(p.recv_node.size());
+  // (+4 B per param for the in-place P2P publish copy of x^(t))
+  const double bytes = double(len) * ((per + (xpub_out ? 4.0 : 0.0)) * p.n_local + remote_hbm);
+  // NVLink bytes the launch reads in-kernel (P2P exchange rounds, in-place P2P ranges)
+  const double nvl = ((transport == DG_TRANSPORT_P2P && !slot_override) || xpub_out)
                          ? 4.0 * double(len) * double(p.recv_node.size())
                          : 0.0;
   timed(bytes, nvl, [&] {
     if (st_k)
-      launch_groups(*tp, x, xo, g, m, v, b, slot_ptr, off, len, s, fold, t, sms_for(p));
+      launch_groups(*tp, x, xo, g, m, v, b, slot_ptr, off, len, s, fold, t, sms_for(p), xpub_out);
     else if (tma)
       dg::launch_tma(p, bf, algo, fold, off, len, s, int(t), flag, comp);
     else
@@ -456,7 +527,7 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
 void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* const* xo,
                                    const float* const* g, float* const* m, float* const* v, float* const* b,
                                    const float* const* slot_ptr, size_t off, size_t len,
-                                   const dg::DevScalars& s, bool fold, long t, int sms) {
+                                   const dg::DevScalars& s, bool fold, long t, int sms, float* const* xp) {
   const int ng = int(tp.groups.size());
   for (int g0 = 0; g0 < ng; g0 += dg::kShGroups) {
     auto& a = sargs;
@@ -472,7 +543,7 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
       for (int j = 0; j < d.nx; ++j) {
         const int c = G.srcs[size_t(j)];
         d.row[j] = c >= 0 ? x[c] + off : slot_ptr[-c - 1];
-        if (c >= 0 || transport != DG_TRANSPORT_P2P) d.local_rows |= 1u << j;
+        if (c >= 0 || (transport != DG_TRANSPORT_P2P && !xp)) d.local_rows |= 1u << j;
         d.wrow[j] = 0.0;
         for (int q = 0; q < d.nl; ++q)
           if (G.w[size_t(q)][size_t(j)] != 0.0) d.wrow[j] = G.w[size_t(q)][size_t(j)];
@@ -480,6 +551,7 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
       for (int q = 0; q < d.nl; ++q) {
         const int li = G.members[size_t(q)];
         d.xo[q] = xo[li] + off;
+        d.xp[q] = xp ? xp[li] + off : nullptr;
         d.g[q] = g[li] + off;
         d.m[q] = m[li] + off;
         d.v[q] = v[li] + off;
@@ -596,6 +668,69 @@ void dg_engine::post_range_exchange(const dg::RoundPlan& q, size_t off, size_t l
   received += 4.0 * double(len) * double(q.recv_node.size());
 }
 
+void dg_engine::signal_range(int slot, unsigned long long value) {
+  // every peer learns "this rank finished iteration value - 1 on the range"
+  if (signal_kernel) {
+    dg::SignalArgs a{};
+    for (int r = 0; r < G; ++r)
+      if (r != rank) a.dst[a.n++] = peer_sig[r] + size_t(slot) * G + rank;
+    a.value = value;
+    dg::signal_peers<<<1, 32, 0, comp>>>(a);
+    CU(cudaGetLastError());
+    return;
+  }
+  for (int r = 0; r < G; ++r)
+    if (r != rank)
+      dg::cu_check(dg::memops().write64(reinterpret_cast<CUstream>(comp),
+                                        reinterpret_cast<CUdeviceptr>(peer_sig[r] + size_t(slot) * G + rank), value,
+                                        CU_STREAM_WRITE_VALUE_DEFAULT),
+                   "cuStreamWriteValue64");
+}
+
+// In-place P2P range update (see the inplace_p2p fields): no copies, no NCCL;
+// the peers' x^(t-1) of the range is read in-kernel over NVLink from their
+// publish buffers.
+void dg_engine::step_range_p2p(long t, size_t off, size_t len) {
+  bool fold = false;
+  const dg::DevScalars s = dg::scalars(&adam, algo, t, T, &fold);
+  CU(cudaSetDevice(device));
+  auto it = range_slot.find(off);
+  if (it == range_slot.end()) {
+    if (int(range_slot.size()) >= kMaxRanges) dg::config_error("step_range: more than 4096 distinct ranges");
+    it = range_slot.emplace(off, int(range_slot.size())).first;
+  }
+  const int slot = it->second;
+  ++steps;
+  const long last = range_last.count(off) ? range_last[off] : -1;
+  if (last != t - 1) {  // first step of this range (or a restart): publish x^(t-1)
+    for (int i = 0; i < NL; ++i)
+      CU(cudaMemcpyAsync(xpub[(t - 1) & 1] + size_t(i) * d_pad + off, buf(DG_BUF_X, i) + off, len * sizeof(float),
+                         cudaMemcpyDeviceToDevice, comp));
+    signal_range(slot, (unsigned long long)t);
+  }
+  fault_delay(comp);
+  // every peer finished iteration t-1 on this range
+  for (int r = 0; r < G; ++r)
+    if (r != rank)
+      dg::cu_check(dg::memops().wait64(reinterpret_cast<CUstream>(comp),
+                                       reinterpret_cast<CUdeviceptr>(sig + size_t(slot) * G + r),
+                                       (cuuint64_t)t, CU_STREAM_WAIT_VALUE_GEQ),
+                   "cuStreamWaitValue64");
+  const dg::RoundPlan& p = plans[size_t((t - 1) % P)];
+  std::vector<const float*> slot_ptr(std::max<size_t>(1, p.recv_node.size()));
+  for (size_t r = 0; r < p.recv_node.size(); ++r) {
+    const int node = p.recv_node[r], owner = dg::owner_of(node, N, G);
+    slot_ptr[r] = peer_base[(t - 1) & 1][owner] + size_t(node - dg::first_node_of(owner, N, G)) * d_pad + off;
+  }
+  float* pub[dg::kMaxLocal];
+  for (int i = 0; i < NL; ++i) pub[i] = xpub[t & 1] + size_t(i) * d_pad;
+  sent += 4.0 * double(len) * double(p.send_node.size());
+  received += 4.0 * double(len) * double(p.recv_node.size());
+  if (!diag_skip_kernel) enqueue_fused(p, off, len, 0, s, fold, t, slot_ptr.data(), pub);
+  signal_range(slot, (unsigned long long)(t + 1));
+  range_last[off] = t;
+}
+
 // U_k of the paper: wait for this range's round-t exchange (posted at t-1 or
 // now), update the range, post its round-(t+1) exchange.
 void dg_engine::step_range(long t, size_t off, size_t len) {
@@ -603,6 +738,7 @@ void dg_engine::step_range(long t, size_t off, size_t len) {
   if (algo == DG_ALGO_ALLREDUCE) dg::config_error("step_range: not available for All-Reduce Adam");
   if (off % dg::kAlign || off >= d || len == 0 || len > d - off)
     dg::config_error("step_range: range must start at a multiple of 64 and lie inside [0, d)");
+  if (inplace_p2p) return step_range_p2p(t, off, len);
   bool fold = false;
   const dg::DevScalars s = dg::scalars(&adam, algo, t, T, &fold);
   CU(cudaSetDevice(device));
@@ -649,6 +785,7 @@ void dg_engine::step(long t) {
   CU(cudaSetDevice(device));
   const size_t ri = size_t((t - 1) % P);
   const dg::RoundPlan& p = plans[ri];
+  if (inplace_p2p) return step_range_p2p(t, 0, d);
   ++steps;
   if (algo == DG_ALGO_ALLREDUCE) return step_allreduce(t, s);
   if (transport == DG_TRANSPORT_P2P && G > 1) {
@@ -865,9 +1002,9 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     }
     e->NL = e->plans[0].n_local;
     e->in_place = (c->flags & DG_ENGINE_IN_PLACE) != 0;
-    e->transport = (c->transport == DG_TRANSPORT_NCCL || e->in_place) ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
+    e->transport = c->transport == DG_TRANSPORT_NCCL ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
     bool auto_transport = c->transport == DG_TRANSPORT_AUTO;
-    if (const char* tr = e->in_place ? nullptr : std::getenv("DG_TRANSPORT")) {
+    if (const char* tr = std::getenv("DG_TRANSPORT")) {
       e->transport = std::string(tr) == "nccl" ? DG_TRANSPORT_NCCL : DG_TRANSPORT_P2P;
       auto_transport = false;
     }
@@ -889,15 +1026,24 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
         all[r].push_back(g == e->rank ? e->plans[r] : dg::build_round_plan(*c->schedule, e->G, g, r + 1));
         e->xshare = e->xshare && dg::build_group_plan(all[r].back()).ok;
       }
+    // P2P exchange rounds (remote x^(t-1) read in-kernel over NVLink) run the
+    // legacy kernels unless DG_XSHARE_REMOTE=1: the x-sharing kernel loads
+    // each row one column block ahead only, which does not cover NVLink
+    // latency (config 3 at 2 GPUs: 19.9 ms vs 9.2 ms, measured)
+    const bool xs_remote = dg::env_int("DG_XSHARE_REMOTE", 0) != 0;
+    e->gplans.resize(size_t(e->P));
     for (int r = 0; r < e->P; ++r) {
       bool pp = false;
+      for (int g = 0; g < e->G; ++g)
+        if (!all[r][g].recv_node.empty()) e->round_remote[r] = 1;
+      const bool xs = e->xshare && (e->in_place || !p2p || !e->round_remote[r] || xs_remote);
+      e->plans[r].xshare = xs;
       for (int g = 0; g < e->G; ++g) {
         const auto& q = all[r][g];
-        if (!e->xshare && ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize)) pp = true;
-        if (!q.recv_node.empty()) e->round_remote[r] = 1;
+        if (!xs && ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize)) pp = true;
       }
-      if (p2p && e->round_remote[r]) pp = true;
-      if (pp && e->xshare) {
+      if (p2p && !e->in_place && e->round_remote[r]) pp = true;  // in place: peers read xpub instead
+      if (pp && xs) {
         // x-sharing kernel: in place on this GPU; only peers' readers (P2P
         // exchange rounds) need x^(t) in the other buffer
         e->plans[r].pingpong = true;
@@ -929,20 +1075,29 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
           if (cp.srcs[k] < 0) ++remote_reads;
       const int ncomp = int(pr.comps.size());
       if (pr.comp_size == 1 && ncomp >= dg::warps_min_nc() && ncomp <= 8) remote_reads = long(pr.recv_node.size());
-      if (e->xshare) {  // each group row is loaded once per column
-        e->gplans.push_back(dg::build_group_plan(pr));
+      if (xs) {  // each group row is loaded once per column
+        e->gplans[size_t(r)] = dg::build_group_plan(pr);
         remote_reads = 0;
-        for (const auto& gr : e->gplans.back().groups)
+        for (const auto& gr : e->gplans[size_t(r)].groups)
           for (int c : gr.srcs) remote_reads += c < 0;
       }
       const char* pv = std::getenv("DG_P2P_PULL");  // 0 never, 1 auto (default), 2 always
       const int pull_mode = pv ? std::atoi(pv) : 1;
       // in-kernel peer loads reach ~770 GB/s, copy-engine pulls ~420 GB/s (measured):
       // pull only when a remote bucket is read >= 1.75x on average
-      pr.pull = p2p && !pr.recv_node.empty() &&
+      pr.pull = p2p && !e->in_place && !pr.recv_node.empty() &&
                 (pull_mode == 2 || (pull_mode == 1 && 4 * remote_reads >= 7 * long(pr.recv_node.size())));
     }
     if (e->NL < 1) dg::config_error("engine_create: no resident nodes on this rank");
+    if (p2p && e->in_place && (!e->xshare || !dg::memops().wait64 || !dg::memops().write64)) {
+      // the publish copy of x^(t) is written by the x-sharing kernel only
+      if (!auto_transport)
+        dg::config_error("engine_create: in-place P2P needs the x-sharing kernel and stream memory operations");
+      e->transport = DG_TRANSPORT_NCCL;
+      p2p = false;
+    }
+    e->inplace_p2p = p2p && e->in_place;
+    e->signal_kernel = dg::env_int("DG_SIGNAL_KERNEL", 0) != 0;
     CU(cudaSetDevice(c->device));
     e->sm_total = dg::sm_count(c->device);
     if (const char* rs = std::getenv("DG_RESERVE_SMS")) e->reserve_sms = std::max(0, std::atoi(rs));
@@ -964,9 +1119,18 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       CU(cudaMalloc(&e->arena[k], sizeof(float) * e->d_pad * e->NL));
       CU(cudaMemsetAsync(e->arena[k], 0, sizeof(float) * e->d_pad * e->NL, e->comp));
     }
-    if (any_pp || p2p) {
+    if ((any_pp || p2p) && !e->in_place) {
       CU(cudaMalloc(&e->x_alt, sizeof(float) * e->d_pad * e->NL));
       CU(cudaMemsetAsync(e->x_alt, 0, sizeof(float) * e->d_pad * e->NL, e->comp));
+    }
+    if (e->inplace_p2p) {
+      for (auto& pb : e->xpub) {
+        CU(cudaMalloc(&pb, sizeof(float) * e->d_pad * e->NL));
+        CU(cudaMemsetAsync(pb, 0, sizeof(float) * e->d_pad * e->NL, e->comp));
+      }
+      const size_t nsig = size_t(dg_engine::kMaxRanges) * e->G;
+      CU(cudaMalloc(&e->sig, sizeof(unsigned long long) * nsig));
+      CU(cudaMemsetAsync(e->sig, 0, sizeof(unsigned long long) * nsig, e->comp));
     }
     bool any_pull = false;
     for (const auto& pr : e->plans) any_pull |= pr.pull;
@@ -995,15 +1159,21 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       NC(ncclCommInitRank(&e->nccl, e->G, id, e->rank));
     }
     for (int b = 0; b < 2; ++b) e->peer_base[b].assign(e->G, nullptr);
-    e->peer_base[0][e->rank] = e->arena[DG_BUF_X];
-    e->peer_base[1][e->rank] = e->x_alt;
+    // exported buffers: x and x_alt, or (in place) the two publish buffers + the flags
+    float* exp0 = e->inplace_p2p ? e->xpub[0] : e->arena[DG_BUF_X];
+    float* exp1 = e->inplace_p2p ? e->xpub[1] : e->x_alt;
+    e->peer_base[0][e->rank] = exp0;
+    e->peer_base[1][e->rank] = exp1;
+    e->peer_sig.assign(e->G, nullptr);
+    e->peer_sig[e->rank] = e->sig;
     if (p2p) {
       // Exchange CUDA IPC handles of both x buffers (one 128-byte record per
       // rank), open the peers', then AGREE on the outcome (all-reduce min of a
       // per-rank success flag) so every rank commits to the same transport.
       // Only CUDA (IPC) failures are tolerated locally; NCCL errors propagate.
       static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
-      std::vector<char> mine(128, 0), all(128 * size_t(e->G));
+      constexpr size_t kRec = 192;  // three handles per rank: exp0, exp1, flags (in place)
+      std::vector<char> mine(kRec, 0), all(kRec * size_t(e->G));
       int ok = 1;
       std::string why;
       auto attempt = [&](auto&& f) {
@@ -1018,15 +1188,16 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
         }
       };
       attempt([&] {
-        CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data()), e->arena[DG_BUF_X]));
-        CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + 64), e->x_alt));
+        CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data()), exp0));
+        CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + 64), exp1));
+        if (e->sig) CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + 128), e->sig));
       });
       char* dbuf = nullptr;
       int* dok = nullptr;
       CU(cudaMalloc(&dbuf, all.size()));
       CU(cudaMalloc(&dok, sizeof(int)));
-      CU(cudaMemcpy(dbuf + 128 * size_t(e->rank), mine.data(), 128, cudaMemcpyHostToDevice));
-      NC(ncclAllGather(dbuf + 128 * size_t(e->rank), dbuf, 128, ncclChar, e->nccl, e->comp));
+      CU(cudaMemcpy(dbuf + kRec * size_t(e->rank), mine.data(), kRec, cudaMemcpyHostToDevice));
+      NC(ncclAllGather(dbuf + kRec * size_t(e->rank), dbuf, kRec, ncclChar, e->nccl, e->comp));
       CU(cudaStreamSynchronize(e->comp));
       CU(cudaMemcpy(all.data(), dbuf, all.size(), cudaMemcpyDeviceToHost));
       attempt([&] {
@@ -1034,10 +1205,17 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
           if (g == e->rank) continue;
           for (int b = 0; b < 2; ++b) {
             cudaIpcMemHandle_t h;
-            std::memcpy(&h, all.data() + 128 * size_t(g) + 64 * b, 64);
+            std::memcpy(&h, all.data() + kRec * size_t(g) + 64 * b, 64);
             void* ptr = nullptr;
             CU(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
             e->peer_base[b][g] = static_cast<float*>(ptr);
+          }
+          if (e->sig) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, all.data() + kRec * size_t(g) + 128, 64);
+            void* ptr = nullptr;
+            CU(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            e->peer_sig[g] = static_cast<unsigned long long*>(ptr);
           }
         }
       });
@@ -1051,12 +1229,18 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
         CU(cudaMalloc(&e->bar_buf, sizeof(float)));
         CU(cudaMemset(e->bar_buf, 0, sizeof(float)));
       } else {
-        for (int g = 0; g < e->G; ++g)
+        for (int g = 0; g < e->G; ++g) {
           for (int b = 0; b < 2; ++b)
             if (g != e->rank && e->peer_base[b][g]) {
               cudaIpcCloseMemHandle(e->peer_base[b][g]);
               e->peer_base[b][g] = nullptr;
             }
+          if (g != e->rank && e->peer_sig[g]) {
+            cudaIpcCloseMemHandle(e->peer_sig[g]);
+            e->peer_sig[g] = nullptr;
+          }
+        }
+        e->inplace_p2p = false;
         // every rank reaches this branch together (agreed flag)
         if (!auto_transport)
           dg::config_error("engine_create: P2P transport unavailable (CUDA IPC failed on some rank" +

@@ -49,6 +49,7 @@ struct ShGroup {
   const float* row[kShRows];          // x^(t-1) source rows (resident, peer or recv slot)
   double wrow[kShRows];               // COLW: the weight every reader of row r uses
   float* xo[kShNodes];                // where member q's x^(t) goes
+  float* xp[kShNodes];                // optional second copy of x^(t) (in-place P2P publish buffer)
   const float* g[kShNodes];
   float* m[kShNodes];
   float* v[kShNodes];
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
   const bool pf_x = conv && (gp.local_rows >> w & 1);  // resident row: prefetchable into L2
   const float* gq = member ? gp.g[w] : nullptr;
   float* xq = member ? gp.xo[w] : nullptr;
+  float* xpq = member ? gp.xp[w] : nullptr;
   float* mq = member ? gp.m[w] : nullptr;
   float* vq = member ? gp.v[w] : nullptr;
   float* bq = member ? gp.b[w] : nullptr;
@@ -263,6 +265,7 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         bad |= !ok;
 #endif
         st4(xq + e, x);
+        if (xpq) st4(xpq + e, x);
         st4_mv(mq + e, m);
         st4_mv(vq + e, v);
       } else {
@@ -283,6 +286,7 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         bad |= !ok;
 #endif
         st4(xq + e, x);
+        if (xpq) st4(xpq + e, x);
         st4_mv(bq + e, bb);
         if (FOLD) {
           st4_mv(mq + e, m);
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         }
       }
       xq[e] = x;
+      if (xpq) xpq[e] = x;
     }
   }
   report_divergence(bad, a.t, a.div_flag);

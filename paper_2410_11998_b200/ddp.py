@@ -14,6 +14,11 @@ has been accumulated, the hook hands the bucket to dg_engine_step_range:
     post the bucket's round-(t+1) exchange                   C_k
 
 so the gossip of bucket k overlaps the rest of backward and the next forward.
+Transport (`transport=`): "auto" (default) = P2P when CUDA IPC works: the
+update kernel reads the peers' x^(t-1) of the bucket in-kernel over NVLink
+from their publish buffers, ordered by per-bucket stream-memory flags (no
+copies, no NCCL kernels); "nccl" = NCCL send/recv of the bucket pre-posted at
+t-1, as described above.
 Buckets launch in a fixed global order (bucket 0, 1, ... on every rank) however
 autograd orders the hooks.  An iteration starts with the first hook of a
 backward and ends at the next forward (which joins the engine's stream);
@@ -28,7 +33,8 @@ from typing import Callable, List, Optional
 
 import torch
 
-from . import (DADAM, ENGINE_IN_PLACE, G, TRANSPORT_NCCL, X, ConfigError, Engine, OptimizerConfig,
+from . import (DADAM, ENGINE_IN_PLACE, G, TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_P2P, X, ConfigError, Engine,
+               OptimizerConfig,
                make_aer, make_complete, make_one_peer_exponential, make_one_peer_ring, make_static_exponential,
                nccl_unique_id)
 
@@ -59,7 +65,7 @@ def _round_up(n: int, a: int = 64) -> int:
 class DecentralizedDataParallel(torch.nn.Module):
     def __init__(self, module: torch.nn.Module, topology="one_peer_exponential",
                  optimizer: Optional[OptimizerConfig] = None, algo: int = DADAM, total_steps: int = 0,
-                 bucket_cap_mb: float = 25.0, aer_workers_per_node: int = 1):
+                 bucket_cap_mb: float = 25.0, aer_workers_per_node: int = 1, transport: str = "auto"):
         super().__init__()
         import torch.distributed as dist
         self.module = module
@@ -103,7 +109,8 @@ class DecentralizedDataParallel(torch.nn.Module):
             nccl_id = obj[0]
         self.engine = Engine(sched, self.d, optimizer or OptimizerConfig(), algo=algo, total_steps=total_steps,
                              world_size=self.world, rank=self.rank, device=self.device, nccl_id=nccl_id,
-                             transport=TRANSPORT_NCCL, flags=ENGINE_IN_PLACE)
+                             transport={"auto": TRANSPORT_AUTO, "p2p": TRANSPORT_P2P,
+                                        "nccl": TRANSPORT_NCCL}[transport], flags=ENGINE_IN_PLACE)
         self._x = device_view(self.engine.buffer(0, X), self.d)
         self._g = device_view(self.engine.buffer(0, G), self.d)
         with torch.no_grad():
@@ -157,8 +164,9 @@ class DecentralizedDataParallel(torch.nn.Module):
             self._drain()
 
     def _drain(self):
-        # Buckets launch strictly in index order on every rank (the exchange is
-        # NCCL point-to-point, matched by issue order), like
+        # Buckets launch strictly in index order on every rank (NCCL
+        # point-to-point is matched by issue order; the P2P
+        # transport assigns per-bucket flags in first-use order), like
         # torch DDP's next_bucket_: a bucket that becomes ready early waits for
         # its predecessors.
         while self._next < len(self.buckets) and self._ready[self._next]:

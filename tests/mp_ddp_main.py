@@ -29,7 +29,8 @@ def main():
         model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.GELU(), torch.nn.Linear(256, 10)).cuda()
         ref_model = copy.deepcopy(model)
         cfg = dg.OptimizerConfig(alpha=1e-3, beta1=0.9, beta2=0.999, eps=1e-8)
-        ddp = DecentralizedDataParallel(model, topology=topo, optimizer=cfg, bucket_cap_mb=0.02)
+        ddp = DecentralizedDataParallel(model, topology=topo, optimizer=cfg, bucket_cap_mb=0.02,
+                                        transport=os.environ.get("MP_DDP_TRANSPORT", "auto"))
         names = {id(p): n for n, p in ddp.module.named_parameters()}
         layout = [((names[id(p)], p.numel()), o) for p, o in ddp._layout]
         ref = ReferenceDAdam(ref_model, layout, ddp.d, ddp.schedule, cfg, world, rank)
@@ -43,7 +44,9 @@ def main():
         got, want = ddp.flat_parameters(), ref.x
         err = float((got.double() - want.double()).norm() / want.double().norm())
         exact = bool(torch.equal(got, want))
-        print(f"rank {rank}: {topo} buckets={len(ddp.buckets)} normwise={err:.3e} bit_exact={exact}", flush=True)
+        tr = {1: "nccl", 2: "p2p"}.get(ddp.engine.stats()["transport"])
+        print(f"rank {rank}: {topo} transport={tr} buckets={len(ddp.buckets)} normwise={err:.3e} bit_exact={exact}",
+              flush=True)
         bad += err > 1e-6
         dist.barrier()
     dist.destroy_process_group()

@@ -102,6 +102,38 @@ def main():
                   f"barriers {stats['barriers']}", flush=True)
             eng.close()
             dist.barrier()
+    # f1 path: in-place engine (x never moves), dg_engine_step_range over three
+    # ranges per iteration -- P2P: peers' publish buffers read in-kernel,
+    # ordered by per-range stream-memory flags; NCCL: pre-posted send/recv
+    cuts = [0, 40000, 70016, d] if d > 70016 else [0, d]
+    for fn, kind, args in [("make_one_peer_exponential", "ONE_PEER_EXP", (8,)),
+                           ("make_static_exponential", "STATIC_EXP", (8,)), ("make_one_peer_ring", "ONE_PEER_RING", (8,))]:
+        for algo in (0, 1):
+            obj = [dg.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            eng = dg.Engine(getattr(dg, fn)(*args), d, dg.OptimizerConfig(**CFG[algo]), algo=algo, total_steps=T,
+                            world_size=world, rank=rank, device=local, nccl_id=obj[0], transport=TRANSPORT,
+                            flags=dg.ENGINE_IN_PLACE)
+            eng.fill_synthetic(dg.X, SEED, dg.Stream.CONSENSUS_INIT, True, 0)
+            for t in range(1, T + 1):
+                eng.fill_synthetic(dg.G, SEED, dg.Stream.MINIBATCH, True, t)
+                for k in range(len(cuts) - 1):
+                    eng.step_range(t, cuts[k], cuts[k + 1] - cuts[k])
+            eng.sync()
+            st = O.init_state(8, d, SEED, True, np.float32, algo)
+            O.run(O.make(getattr(O, kind), *args), algo, O.OptimizerConfig(**CFG[algo]), SEED, st, 1, T, T)
+            f = eng.first_node
+            keys = [("x", dg.X), ("m", dg.M), ("v", dg.V)] + ([("b", dg.ACC)] if algo else [])
+            for k, w in keys:
+                got = np.stack([eng.download(i, w) for i in range(eng.local_nodes)])
+                if not np.array_equal(got.view(np.uint32), st[k][f:f + eng.local_nodes].view(np.uint32)):
+                    print(f"rank {rank}: MISMATCH in-place {fn}{args} algo={algo} {k}", flush=True)
+                    bad += 1
+            stats = eng.stats()
+            print(f"rank {rank}: in-place {fn}{args} algo={algo} transport={stats['transport']} ranges={len(cuts) - 1}"
+                  f" launches {stats['kernel_launches']}", flush=True)
+            eng.close()
+            dist.barrier()
     # f3: All-Reduce Adam across ranks (NCCL all-reduce of fp64 gradient column sums)
     for n_nodes in (8, 16):
         obj = [dg.nccl_unique_id() if rank == 0 else None]

@@ -80,11 +80,14 @@ def test_fullsize_configs_4_and_5(transport):
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
 
 
-def test_ddp_multigpu():
-    """f1: the grad-hook wrapper (per-bucket NCCL exchange posted for the next
-    iteration) matches a plain-PyTorch decentralized Adam on 2-4 GPUs."""
+@pytest.mark.parametrize("transport", ["auto", "nccl"])
+def test_ddp_multigpu(transport):
+    """f1: the grad-hook wrapper (per-bucket exchange: in-place P2P reads of the
+    peers' publish buffers, or NCCL send/recv posted for the next iteration)
+    matches a plain-PyTorch decentralized Adam on 2-4 GPUs."""
     world = min(4, torch.cuda.device_count())
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_ddp_main.py")]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    p = subprocess.run(cmd, env={**os.environ, "MP_DDP_TRANSPORT": transport}, capture_output=True, text=True,
+                       timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
