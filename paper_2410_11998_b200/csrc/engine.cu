@@ -529,6 +529,15 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
                                    const float* const* slot_ptr, size_t off, size_t len,
                                    const dg::DevScalars& s, bool fold, long t, int sms, float* const* xp) {
   const int ng = int(tp.groups.size());
+#if DG_XS_IDX32
+  const size_t piece = size_t(1) << 30;  // the kernel indexes columns in 32 bits
+#else
+  const size_t piece = len;
+#endif
+  const size_t len_all = len, off_all = off;
+  for (size_t o2 = 0; o2 < len_all; o2 += piece) {
+  off = off_all + o2;
+  len = std::min(piece, len_all - o2);
   for (int g0 = 0; g0 < ng; g0 += dg::kShGroups) {
     auto& a = sargs;
     std::memset(&a, 0, sizeof(a));
@@ -542,7 +551,7 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
       warps = std::max(warps, std::max(d.nl, d.nx));  // a warp per member and per source row
       for (int j = 0; j < d.nx; ++j) {
         const int c = G.srcs[size_t(j)];
-        d.row[j] = c >= 0 ? x[c] + off : slot_ptr[-c - 1];
+        d.row[j] = c >= 0 ? x[c] + off : slot_ptr[-c - 1] + o2;
         if (c >= 0 || (transport != DG_TRANSPORT_P2P && !xp)) d.local_rows |= 1u << j;
         d.wrow[j] = 0.0;
         for (int q = 0; q < d.nl; ++q)
@@ -578,6 +587,7 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
     a.contiguous = dg::env_int("DG_XS_CONTIG", 0) != 0;
     a.div_flag = flag;
     dg::launch_xshare(a, cnt, warps, tp.max_deg, tp.colw, algo, fold, sms, comp);
+  }
   }
 }
 

@@ -25,10 +25,11 @@
 // busy at the HBM roofline.  Here a thread holds one member's 4-5 float4
 // streams: 3 CTAs of 8 warps per SM.  Every lane prefetches its streams into
 // L2 (prefetch.global.L2) DG_PREFETCH column blocks ahead, so the demand loads
-// mostly hit L2, and the x^(t-1) row is loaded one column block ahead (4
-// registers), so the conversion never waits on DRAM: the latency is covered
-// without holding a second copy of g, m, v in registers.  Non-finite results
-// are detected by an FFMA-by-zero accumulator (nan_acc), one vote per launch.
+// mostly hit L2: the DRAM latency is covered without registers.  Non-finite
+// results are detected by an FFMA-by-zero accumulator (nan_acc), one vote per
+// launch.  Measured (config 3, kernel fraction of the HBM copy): lane-0 bulk
+// prefetch 0.84 -> per-lane prefetch 0.87; loading x one column block ahead
+// (DG_XS_XPIPE=1) 0.78.
 //
 // Jacobi snapshot: every read of a column's x rows (step 1)
 // precedes the barrier, every x^(t) store of that column (step 3) follows it,
@@ -92,7 +93,17 @@ __device__ __forceinline__ void prefetch_l2_line(const void* p) {
 #define DG_XS_NANACC 1  // non-finite detection by FFMA-by-zero accumulation (0: isfinite)
 #endif
 #ifndef DG_XS_XPIPE
-#define DG_XS_XPIPE 1   // x^(t-1) rows loaded one column block ahead (0: just in time)
+#define DG_XS_XPIPE 0   // 1: x^(t-1) rows loaded one column block ahead (measured slower: 0.78 vs 0.87)
+#endif
+
+#ifndef DG_XS_FASTDIV
+#define DG_XS_FASTDIV 0  // 1: branch-free 4-wide Adam direction (adam_dir4)
+#endif
+#ifndef DG_XS_STAGE
+#define DG_XS_STAGE 0    // > 0: x rows staged that many column blocks ahead (cp.async ring)
+#endif
+#ifndef DG_XS_IDX32
+#define DG_XS_IDX32 0    // 1: 32-bit column indices (the host splits launches at 2^30 elements)
 #endif
 
 #ifndef DG_XS_MINB
@@ -106,17 +117,23 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
   const int nl = gp.nl, nx = gp.nx;
   const bool member = w < nl;  // warp w updates member w ...
   const bool conv = w < nx;    // ... and converts source row w
-  const long long n4 = a.n >> 2;
+#if DG_XS_IDX32
+  using idx_t = unsigned;  // a.n < 2^31 (launch_groups splits longer ranges)
+#else
+  using idx_t = long long;
+#endif
+  const idx_t nn = idx_t(a.n);
+  const idx_t n4 = nn >> 2;
   // column blocks of this CTA: blk = first + i * step, i < count -- grid-stride
   // (default: at any moment the CTAs sweep one compact window of every
   // stream, so DRAM rows are used whole) or one contiguous range per CTA
-  const long long nblk = (n4 + 31) >> 5;
-  long long first, step, count;
+  const idx_t nblk = (n4 + 31) >> 5;
+  idx_t first, step, count;
   if (a.contiguous) {
-    const long long per = (nblk + gridDim.x - 1) / gridDim.x;
-    first = (long long)blockIdx.x * per;
+    const idx_t per = (nblk + gridDim.x - 1) / gridDim.x;
+    first = idx_t(blockIdx.x) * per;
     step = 1;
-    count = max(0LL, min(nblk, first + per) - first);
+    count = first < nblk ? min(nblk, first + per) - first : idx_t(0);
   } else {
     first = blockIdx.x;
     step = gridDim.x;
@@ -151,11 +168,11 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
   // operand must be uniform, so the compiler wraps each in a waterfall loop:
   // ~90 instructions per column block, measured).
   const int pd = a.prefetch;
-  auto prefetch = [&](long long i) {
+  auto prefetch = [&](idx_t i) {
     if (i >= count) return;
 #if DG_XS_PF
-    const long long pe = (((first + i * step) << 5) + lane) << 2;
-    if (pe >= a.n) return;
+    const idx_t pe = (((first + i * step) << 5) + lane) << 2;
+    if (pe >= nn) return;
     if (member) {
       prefetch_l2_line(gq + pe);
       prefetch_l2_line(mq + pe);
@@ -165,8 +182,8 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
     if (pf_x) prefetch_l2_line(xr + pe);
 #else
     if (lane != 0) return;
-    const long long e = (first + i * step) << 7;  // first element of the block
-    const uint32_t bytes = uint32_t(min(128LL, ((a.n - e) + 3) & ~3LL)) * 4u;
+    const idx_t e = (first + i * step) << 7;  // first element of the block
+    const uint32_t bytes = uint32_t(min(idx_t(128), ((nn - e) + 3) & ~idx_t(3))) * 4u;
     if (member) {
       prefetch_l2(gq + e, bytes);
       prefetch_l2(mq + e, bytes);
@@ -183,20 +200,41 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
   bool bad = false;
   int buf = 0;
   const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#if DG_XS_STAGE
+  // x^(t-1) rows staged DG_XS_STAGE column blocks ahead with cp.async into a
+  // per-lane shared-memory ring (no registers held; peer rows over NVLink
+  // have microseconds to arrive).  Each lane reads back only the 16 B it
+  // copied itself, so cp.async.wait_group is the only synchronisation.
+  constexpr int kSlots = DG_XS_STAGE + 2;
+  __shared__ __align__(16) float4 XR[kShRows * kSlots * 32];
+  const uint32_t xr_base = uint32_t(__cvta_generic_to_shared(&XR[(w * kSlots) * 32 + lane]));
+  auto stage = [&](idx_t i) {  // issue block i of this warp's row (one commit group per block)
+    if (conv && i < count) {
+      const idx_t qi = ((first + i * step) << 5) + lane;
+      const uint32_t dst = xr_base + uint32_t(i % kSlots) * 32u * 16u;
+      const float* src = qi < n4 ? xr + (qi << 2) : xr;
+      const int bytes = qi < n4 ? 16 : 0;  // zero-fill past the end
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int j = 0; j < DG_XS_STAGE; ++j) stage(idx_t(j));
+#endif
 #if DG_XS_XPIPE
   // x^(t-1) row loaded one column block ahead: the conversion below never
   // waits on DRAM, so the warps reach the barrier together
   float4 xnext = zero4;
   if (conv && count > 0) {
-    const long long q0 = (first << 5) + lane;
+    const idx_t q0 = (first << 5) + lane;
     if (q0 < n4) xnext = ld4(xr + (q0 << 2));
   }
 #endif
-  for (long long i = 0; i < count; ++i, buf ^= 1) {
+  for (idx_t i = 0; i < count; ++i, buf ^= 1) {
     prefetch(i + pd);
-    const long long q = ((first + i * step) << 5) + lane;
+    const idx_t q = ((first + i * step) << 5) + lane;
     const bool live = q < n4;  // false only for lanes of the last column block
-    const long long e = q << 2;
+    const idx_t e = q << 2;
     float4 g, m, v, bb;
     if (member && live) {
       g = ld_stream(gq + e);
@@ -205,11 +243,17 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
       if (ALGO == 1) bb = ld4(bq + e);
     }
     double2* Pb = P + buf * kShBufD2;
+#if DG_XS_STAGE
+    stage(i + DG_XS_STAGE);
+    asm volatile("cp.async.wait_group %0;" ::"n"(DG_XS_STAGE) : "memory");  // block i has landed
+#endif
     if (conv) {
-#if DG_XS_XPIPE
+#if DG_XS_STAGE
+      const float4 x = XR[(w * kSlots + int(i % kSlots)) * 32 + lane];
+#elif DG_XS_XPIPE
       const float4 x = xnext;
       if (i + 1 < count) {
-        const long long q1 = ((first + (i + 1) * step) << 5) + lane;
+        const idx_t q1 = ((first + (i + 1) * step) << 5) + lane;
         xnext = q1 < n4 ? ld4(xr + (q1 << 2)) : zero4;
       }
 #else
@@ -249,10 +293,14 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
       float4 x;
       if (ALGO == 0) {
 #if DG_XS_NANACC
+#if DG_XS_FASTDIV
+        dadam4(mx, g, x, m, v, a.s);
+#else
         dadam_core(mx.x, g.x, x.x, m.x, v.x, a.s);
         dadam_core(mx.y, g.y, x.y, m.y, v.y, a.s);
         dadam_core(mx.z, g.z, x.z, m.z, v.z, a.s);
         dadam_core(mx.w, g.w, x.w, m.w, v.w, a.s);
+#endif
         nan_acc(z, x.x, m.x, v.x);
         nan_acc(z, x.y, m.y, v.y);
         nan_acc(z, x.z, m.z, v.z);
@@ -270,10 +318,14 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         st4_mv(vq + e, v);
       } else {
 #if DG_XS_NANACC
+#if DG_XS_FASTDIV
+        accum4<FOLD>(mx, g, x, m, v, bb, a.s);
+#else
         accum_core<FOLD>(mx.x, g.x, x.x, m.x, v.x, bb.x, a.s);
         accum_core<FOLD>(mx.y, g.y, x.y, m.y, v.y, bb.y, a.s);
         accum_core<FOLD>(mx.z, g.z, x.z, m.z, v.z, bb.z, a.s);
         accum_core<FOLD>(mx.w, g.w, x.w, m.w, v.w, bb.w, a.s);
+#endif
         nan_acc(z, x.x, m.x, v.x);
         nan_acc(z, x.y, m.y, v.y);
         nan_acc(z, x.z, m.z, v.z);
@@ -298,13 +350,16 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
 #if DG_XS_NANACC
   bad = z != z;
 #endif
+#if DG_XS_STAGE
+  asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
   // scalar tail (n % 4 elements): CTA 0, lane l of member warp w takes element
   // n4*4 + l; all x reads precede the barrier, all writes follow it
-  const long long tail0 = n4 << 2;
-  if (blockIdx.x == 0 && tail0 < a.n) {
+  const idx_t tail0 = n4 << 2;
+  if (blockIdx.x == 0 && tail0 < nn) {
     __syncthreads();  // the last column block's table reads are done
-    const long long e = tail0 + lane;
-    const bool t_live = lane < a.n - tail0;
+    const idx_t e = tail0 + lane;
+    const bool t_live = idx_t(lane) < nn - tail0;
     if (conv) {
       const double xe = t_live ? double(xr[e]) : 0.0;
       P[w * kShRowD2 + lane] = make_double2(COLW ? __dmul_rn(wr, xe) : xe, 0.0);

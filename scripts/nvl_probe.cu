@@ -1,0 +1,163 @@
+// nvl_probe.cu -- single-process, two-GPU harness for NVLink evidence of the
+// exchange-round fused kernels (ncu may not wrap a multi-rank command, so the
+// rank-0 side of an exchange round is reproduced here in one process).
+//
+// GPU 0 holds 4 resident nodes (x, g, m, v and the second x buffer); GPU 1
+// holds the 4 remote neighbours' x^(t-1).  Round = one-peer exponential hop 4
+// over 8 nodes on 2 GPUs (BASELINE config 2 at 2 GPUs): node i mixes with
+// node i + 4, weights 1/2, every source pair crosses NVLink.  The kernels are
+// the engine's own templates, launched as the engine launches them for a P2P
+// exchange round (x^(t) to the other buffer):
+//   legacy   gossip_adam_fused<1,2,DAdam>: 4 single-member components,
+//            sources {local i, peer i+4}   (default for P2P exchange rounds)
+//   xshare   gossip_adam_xshare<2,DAdam,COLW>: one group, 4 members, 8 rows
+//            (DG_XSHARE_REMOTE=1, and the in-place P2P transport)
+// plus the same launches with the peer rows replaced by local copies, which
+// isolates the NVLink cost.  Prints GB/s per kernel (CUDA events); under
+//   ncu --metrics nvlrx__bytes.sum,nvltx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
+// the NVLink counters come from hardware.
+//   nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo --expt-relaxed-constexpr \
+//        -I include -I paper_2410_11998_b200/csrc -o build/nvl_probe scripts/nvl_probe.cu
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "xshare.cuh"
+
+#define CK(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) {                                                            \
+      std::fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+      std::exit(1);                                                                     \
+    }                                                                                   \
+  } while (0)
+
+using namespace dg;
+
+int main(int argc, char** argv) {
+  const long long d = argc > 1 ? atoll(argv[1]) : 125000000LL;  // params per node
+  const int iters = argc > 2 ? atoi(argv[2]) : 5;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (ndev < 2) {
+    std::fprintf(stderr, "needs 2 GPUs\n");
+    return 2;
+  }
+  int can = 0;
+  CK(cudaDeviceCanAccessPeer(&can, 0, 1));
+  if (!can) {
+    std::fprintf(stderr, "no peer access 0 -> 1\n");
+    return 2;
+  }
+  CK(cudaSetDevice(0));
+  CK(cudaDeviceEnablePeerAccess(1, 0));
+  const size_t bytes = size_t(d) * sizeof(float);
+  float *xr[4], *xl[4], *xrl[4], *g[4], *m[4], *v[4], *xo[4];
+  CK(cudaSetDevice(1));
+  for (int i = 0; i < 4; ++i) {
+    CK(cudaMalloc(&xr[i], bytes));  // remote neighbours i + 4 on GPU 1
+    CK(cudaMemset(xr[i], 0, bytes));
+  }
+  CK(cudaSetDevice(0));
+  for (int i = 0; i < 4; ++i) {
+    for (float** p : {&xl[i], &xrl[i], &g[i], &m[i], &v[i], &xo[i]}) {
+      CK(cudaMalloc(p, bytes));
+      CK(cudaMemset(*p, 0, bytes));
+    }
+  }
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  DevScalars s{0.974f, 0.026f, 0.999f, 0.001f, 1.0f, 1.0f, -2e-3f, 1e-8f, 1.0f, 0.999f, 0.001f};
+  int* flag = nullptr;
+  CK(cudaMalloc(&flag, sizeof(int)));
+  CK(cudaMemset(flag, 0x7f, sizeof(int)));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+
+  for (int remote = 1; remote >= 0; --remote) {
+    float* const* other = remote ? xr : xrl;
+    // ---- legacy: 4 components of one member, sources {i, i+4}
+    {
+      FusedArgs<1, 2> a{};
+      for (int c = 0; c < 4; ++c) {
+        a.src[c][0] = xl[c];
+        a.src[c][1] = other[c];
+        a.w[c][0][0] = a.w[c][0][1] = 0.5;
+        a.ns[c] = 2;
+        a.nm[c] = 1;
+        a.x[c][0] = xo[c];
+        a.g[c][0] = g[c];
+        a.m[c][0] = m[c];
+        a.v[c][0] = v[c];
+      }
+      a.s = s;
+      a.n = d;
+      a.t = 1;
+      a.div_flag = flag;
+      auto k = gossip_adam_fused<1, 2, 0, false>;
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, LaunchShape<1, 2>::threads, 0));
+      dim3 grid(unsigned(occ * sms / 4), 4);
+      k<<<grid, LaunchShape<1, 2>::threads>>>(a);  // warm-up
+      CK(cudaEventRecord(e0));
+      for (int it = 0; it < iters; ++it) k<<<grid, LaunchShape<1, 2>::threads>>>(a);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      ms /= iters;
+      const double hbm = 4.0 * d * (28.0 + (remote ? 0.0 : 4.0)), nvl = remote ? 4.0 * d * 4.0 : 0.0;
+      std::printf("legacy gossip_adam_fused<1,2> %s: %.3f ms  local HBM %.0f GB/s  NVLink %.0f GB/s\n",
+                  remote ? "peer rows (NVLink)" : "local rows       ", ms, hbm / ms / 1e6, nvl / ms / 1e6);
+    }
+    // ---- x-sharing: one group, 4 members, rows {0,1,2,3 local, 4..7 peer}
+    {
+      ShArgs a{};
+      ShGroup& G = a.grp[0];
+      G.nl = 4;
+      G.nx = 8;
+      for (int r = 0; r < 4; ++r) {
+        G.row[r] = xl[r];
+        G.row[4 + r] = other[r];
+        G.wrow[r] = G.wrow[4 + r] = 0.5;
+      }
+      G.local_rows = remote ? 0x0fu : 0xffu;
+      for (int q = 0; q < 4; ++q) {
+        G.xo[q] = xo[q];
+        G.g[q] = g[q];
+        G.m[q] = m[q];
+        G.v[q] = v[q];
+        G.deg[q] = 2;
+        G.src[q][0] = (unsigned char)q;
+        G.src[q][1] = (unsigned char)(4 + q);
+        for (int k2 = 2; k2 < kShDeg; ++k2) G.src[q][k2] = (unsigned char)kShRows;
+      }
+      a.s = s;
+      a.n = d;
+      a.t = 1;
+      a.prefetch = 1;
+      a.div_flag = flag;
+      auto k = gossip_adam_xshare<2, 0, false, true>;
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0));
+      dim3 grid(unsigned(occ * sms), 1);
+      k<<<grid, 256>>>(a);
+      CK(cudaEventRecord(e0));
+      for (int it = 0; it < iters; ++it) k<<<grid, 256>>>(a);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      ms /= iters;
+      const double hbm = 4.0 * d * (28.0 + (remote ? 0.0 : 4.0)), nvl = remote ? 4.0 * d * 4.0 : 0.0;
+      std::printf("xshare gossip_adam_xshare<2>  %s: %.3f ms  local HBM %.0f GB/s  NVLink %.0f GB/s\n",
+                  remote ? "peer rows (NVLink)" : "local rows       ", ms, hbm / ms / 1e6, nvl / ms / 1e6);
+    }
+  }
+  CK(cudaDeviceSynchronize());
+  return 0;
+}
