@@ -96,14 +96,20 @@ __device__ __forceinline__ void prefetch_l2_line(const void* p) {
 #define DG_XS_XPIPE 0   // 1: x^(t-1) rows loaded one column block ahead (measured slower: 0.78 vs 0.87)
 #endif
 
+// Measured (bench.py kernel fraction of the HBM copy, B200; sweep in
+// profiles/r2_xshare_sweep.md):            config 3  config 2  static accum  AER accum
+//   64-bit indices, IEEE div/sqrt calls      0.873     0.932     0.914         0.953
+//   + 32-bit indices                         0.897     0.934     0.923         0.963
+//   + branch-free Adam direction             0.908     0.920     0.933         0.959
+// so the branch-free direction is used from 4 neighbours up (DG_XS_FASTDIV=2).
 #ifndef DG_XS_FASTDIV
-#define DG_XS_FASTDIV 0  // 1: branch-free 4-wide Adam direction (adam_dir4)
+#define DG_XS_FASTDIV 2  // 1: branch-free 4-wide Adam direction (adam_dir4); 2: when DEG >= 4; 0: never
 #endif
 #ifndef DG_XS_STAGE
 #define DG_XS_STAGE 0    // > 0: x rows staged that many column blocks ahead (cp.async ring)
 #endif
 #ifndef DG_XS_IDX32
-#define DG_XS_IDX32 0    // 1: 32-bit column indices (the host splits launches at 2^30 elements)
+#define DG_XS_IDX32 1    // 1: 32-bit column indices (the host splits launches at 2^30 elements)
 #endif
 
 #ifndef DG_XS_MINB
@@ -112,6 +118,7 @@ __device__ __forceinline__ void prefetch_l2_line(const void* p) {
 template <int DEG, int ALGO, bool FOLD, bool COLW>
 __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(const __grid_constant__ ShArgs a) {
   __shared__ double2 P[2 * kShBufD2];
+  constexpr bool kFastDir = DG_XS_FASTDIV == 1 || (DG_XS_FASTDIV == 2 && DEG >= 4);
   const ShGroup& gp = a.grp[blockIdx.y];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nl = gp.nl, nx = gp.nx;
@@ -293,14 +300,14 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
       float4 x;
       if (ALGO == 0) {
 #if DG_XS_NANACC
-#if DG_XS_FASTDIV
-        dadam4(mx, g, x, m, v, a.s);
-#else
+        if (kFastDir) {
+          dadam4(mx, g, x, m, v, a.s);
+        } else {
         dadam_core(mx.x, g.x, x.x, m.x, v.x, a.s);
         dadam_core(mx.y, g.y, x.y, m.y, v.y, a.s);
         dadam_core(mx.z, g.z, x.z, m.z, v.z, a.s);
         dadam_core(mx.w, g.w, x.w, m.w, v.w, a.s);
-#endif
+        }
         nan_acc(z, x.x, m.x, v.x);
         nan_acc(z, x.y, m.y, v.y);
         nan_acc(z, x.z, m.z, v.z);
@@ -318,14 +325,14 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         st4_mv(vq + e, v);
       } else {
 #if DG_XS_NANACC
-#if DG_XS_FASTDIV
-        accum4<FOLD>(mx, g, x, m, v, bb, a.s);
-#else
+        if (kFastDir) {
+          accum4<FOLD>(mx, g, x, m, v, bb, a.s);
+        } else {
         accum_core<FOLD>(mx.x, g.x, x.x, m.x, v.x, bb.x, a.s);
         accum_core<FOLD>(mx.y, g.y, x.y, m.y, v.y, bb.y, a.s);
         accum_core<FOLD>(mx.z, g.z, x.z, m.z, v.z, bb.z, a.s);
         accum_core<FOLD>(mx.w, g.w, x.w, m.w, v.w, bb.w, a.s);
-#endif
+        }
         nan_acc(z, x.x, m.x, v.x);
         nan_acc(z, x.y, m.y, v.y);
         nan_acc(z, x.z, m.z, v.z);

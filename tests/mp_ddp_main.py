@@ -47,7 +47,8 @@ def main():
         tr = {1: "nccl", 2: "p2p"}.get(ddp.engine.stats()["transport"])
         print(f"rank {rank}: {topo} transport={tr} buckets={len(ddp.buckets)} normwise={err:.3e} bit_exact={exact}",
               flush=True)
-        bad += err > 1e-6
+        # the reference uses the same separate fp32 ops and fp64 mixing: bit-identical by construction
+        bad += (err > 1e-6) or not exact
         dist.barrier()
     dist.destroy_process_group()
     print(f"rank {rank}: {'ok' if not bad else 'FAIL'}", flush=True)
