@@ -20,6 +20,9 @@ if not torch.cuda.is_available():
     ("config2_accum_125M", "make_one_peer_exponential", "ONE_PEER_EXP", (8,), 125_000_000, 1, 100),
     ("config3_static_exp_350M", "make_static_exponential", "STATIC_EXP", (8,), 350_000_000, 0, 100),
     ("config3_accum_350M", "make_static_exponential", "STATIC_EXP", (8,), 350_000_000, 1, 100),
+    # > 2^30 elements per bucket: the x-sharing launch is split into 2^30-element
+    # pieces (32-bit column indices), odd size so the last piece has a scalar tail
+    ("split_2x1.1B", "make_one_peer_exponential", "ONE_PEER_EXP", (2,), 1_100_000_003, 1, 8),
 ])
 def test_fullsize_single_gpu(dg, oracle, name, fn, kind, args, d, algo, T):
     cols = sample_columns(d)
