@@ -1041,12 +1041,22 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     // each row one column block ahead only, which does not cover NVLink
     // latency (config 3 at 2 GPUs: 19.9 ms vs 9.2 ms, measured)
     const bool xs_remote = dg::env_int("DG_XSHARE_REMOTE", 0) != 0;
+    // Rounds whose mixing components are all pairs (one-peer topologies) run the
+    // legacy pair kernel unless DG_XSHARE_PAIRS=1: a pair's two rows are read
+    // by one thread anyway, and without the per-column CTA barrier the small
+    // buckets run faster (config 1, 8 x 2^20: 44.3 vs 49.6 us per step; config
+    // 2 at 125M: 0.93 either way, measured).  In-place engines keep the
+    // x-sharing kernel everywhere (it writes the P2P publish copy).
+    const bool xs_pairs = dg::env_int("DG_XSHARE_PAIRS", 0) != 0;
     e->gplans.resize(size_t(e->P));
     for (int r = 0; r < e->P; ++r) {
-      bool pp = false;
-      for (int g = 0; g < e->G; ++g)
+      bool pp = false, pairs = true;
+      for (int g = 0; g < e->G; ++g) {
         if (!all[r][g].recv_node.empty()) e->round_remote[r] = 1;
-      const bool xs = e->xshare && (e->in_place || !p2p || !e->round_remote[r] || xs_remote);
+        for (const auto& cp : all[r][g].comps) pairs = pairs && cp.members.size() <= 2 && cp.srcs.size() <= 2;
+      }
+      const bool xs = e->xshare && (e->in_place || ((!p2p || !e->round_remote[r] || xs_remote) &&
+                                                    (!pairs || xs_pairs)));
       e->plans[r].xshare = xs;
       for (int g = 0; g < e->G; ++g) {
         const auto& q = all[r][g];

@@ -231,11 +231,10 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
 #if DG_XS_XPIPE
   // x^(t-1) row loaded one column block ahead: the conversion below never
   // waits on DRAM, so the warps reach the barrier together
+  // (addresses clamped to the last column instead of selecting zeros: a
+  // select on the loaded value would wait for the load right away)
   float4 xnext = zero4;
-  if (conv && count > 0) {
-    const idx_t q0 = (first << 5) + lane;
-    if (q0 < n4) xnext = ld4(xr + (q0 << 2));
-  }
+  if (conv && count > 0) xnext = ld4(xr + (min((first << 5) + lane, n4 - 1) << 2));
 #endif
   for (idx_t i = 0; i < count; ++i, buf ^= 1) {
     prefetch(i + pd);
@@ -259,10 +258,7 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
       const float4 x = XR[(w * kSlots + int(i % kSlots)) * 32 + lane];
 #elif DG_XS_XPIPE
       const float4 x = xnext;
-      if (i + 1 < count) {
-        const idx_t q1 = ((first + (i + 1) * step) << 5) + lane;
-        xnext = q1 < n4 ? ld4(xr + (q1 << 2)) : zero4;
-      }
+      if (i + 1 < count) xnext = ld4(xr + (min(((first + (i + 1) * step) << 5) + lane, n4 - 1) << 2));
 #else
       const float4 x = live ? ld4(xr + e) : zero4;
 #endif

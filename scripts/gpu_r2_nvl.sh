@@ -19,14 +19,15 @@ rows=[r for r in csv.reader(open('gpurun_out/r2_nvl_probe_ncu.csv')) if len(r)>1
 for r in rows:
     print(r[0], r[4][:40], r[-3], r[-1])
 PY
-for v in libdg_xs_st2 libdg_xs_st4 libdg_xs_st4_fd_i32; do
+for v in default libdg_xs_xp1 libdg_xs_st1 libdg_xs_st2; do
+  lib=build/variants/$v.so; [ $v = default ] && lib=paper_2410_11998_b200/libdg.so
   for c in 2 3 4; do
-    DG_LIB=build/variants/$v.so DG_XSHARE_REMOTE=1 timeout 900 $TR --master-port 29631 bench.py --gpus $N --config $c --no-e2e --steps 20 \
+    DG_LIB=$lib DG_XSHARE_REMOTE=1 DG_XSHARE_PAIRS=1 timeout 900 $TR --master-port 29631 bench.py --gpus $N --config $c --no-e2e --steps 20 \
       2>&1 | grep "^{" | python -c "
 import json,sys
 for l in sys.stdin:
     j=json.loads(l); print('$v config $c', 'ms', round(j['ms_per_step'],3), 'kfrac', round(j['roofline']['frac'],3), 'step', round(j['step_roofline']['frac'],3), 'nvl(events)', round((j.get('nvlink') or {}).get('achieved') or 0))
 "
   done
-  DG_LIB=build/variants/$v.so timeout 300 $TR --master-port 29632 scripts/xchg_bw.py --range --transport p2p --tag "$v" 2>&1 | grep -E "^xchg|rror" | head -2
+  DG_LIB=$lib timeout 300 $TR --master-port 29632 scripts/xchg_bw.py --range --transport p2p --tag "$v" 2>&1 | grep -E "^xchg|rror" | head -2
 done
