@@ -488,7 +488,7 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
     slot_ptr[r] = slot_override                  ? slot_override[r]
                   : transport == DG_TRANSPORT_P2P ? peer_x(p.recv_node[r]) + off
                                                   : slots + (size_t(slot_set) * max_recv + r) * chunk;
-  const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr};
+  const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr, xpub_out};
   const bool st_k = p.xshare;
   const bool tma = !st_k && dg::use_tma(p);
   dg::LaunchFn fn = nullptr;
@@ -1055,8 +1055,12 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
         if (!all[r][g].recv_node.empty()) e->round_remote[r] = 1;
         for (const auto& cp : all[r][g].comps) pairs = pairs && cp.members.size() <= 2 && cp.srcs.size() <= 2;
       }
-      const bool xs = e->xshare && (e->in_place || ((!p2p || !e->round_remote[r] || xs_remote) &&
-                                                    (!pairs || xs_pairs)));
+      // in place, pair rounds may also run the legacy pair kernel (it writes the
+      // publish copy too) as long as the plain per-thread kernel is the one picked
+      const bool plain_pairs = pairs && !xs_pairs && !dg::use_tma(e->plans[r]) &&
+                               (e->plans[r].comp_size == 2 || int(e->plans[r].comps.size()) < dg::warps_min_nc());
+      const bool xs = e->xshare && (e->in_place ? !plain_pairs
+                                                : ((!p2p || !e->round_remote[r] || xs_remote) && (!pairs || xs_pairs)));
       e->plans[r].xshare = xs;
       for (int g = 0; g < e->G; ++g) {
         const auto& q = all[r][g];

@@ -6,6 +6,12 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 N=$(nvidia-smi -L | wc -l)
 TR="python -m torch.distributed.run --nnodes 1 --nproc-per-node $N --master-addr 127.0.0.1"
+# in-place P2P with the legacy pair kernel writing the publish copy: parity (+fault), DDP
+MP_TRANSPORT=p2p MP_D=100003 MP_CHUNK=16384 timeout 900 $TR --master-port 29641 tests/mp_parity_main.py \
+   > gpurun_out/r2c_parity_p2p.log 2>&1; echo "parity p2p rc=$?"; grep -E "MISMATCH|in-place" gpurun_out/r2c_parity_p2p.log | head -6
+MP_TRANSPORT=p2p MP_D=100003 DG_FAULT_DELAY_US=5000 DG_FAULT_POISON=1 timeout 900 $TR --master-port 29642 \
+   tests/mp_parity_main.py > gpurun_out/r2c_parity_p2p_fault.log 2>&1; echo "parity p2p+fault rc=$?"
+timeout 900 $TR --master-port 29643 tests/mp_ddp_main.py > gpurun_out/r2c_ddp.log 2>&1; echo "ddp rc=$?"; grep rank gpurun_out/r2c_ddp.log | head -3
 for st in 0 4; do
   timeout 300 build/nvl_probe_st$st 125000000 5 > gpurun_out/r2_nvl_probe_st$st.log 2>&1; echo "probe st$st rc=$?"; cat gpurun_out/r2_nvl_probe_st$st.log
 done
