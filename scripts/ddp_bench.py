@@ -2,7 +2,10 @@
 one process per GPU.  Model: MLP stack (fp32 master weights, bf16 autocast
 matmuls).  Modes, each timed over --iters iterations (max over ranks):
   gossip      DecentralizedDataParallel, 25 MB buckets: bucket updates start
-              inside backward, next-iteration exchanges pre-posted
+              inside backward; default transport (in-place P2P: peers' buckets read
+              in-kernel over NVLink, per-bucket stream-memory flags)
+  gossip_nccl same with the NCCL transport (next-iteration send/recv pre-posted,
+              PAPER.md:302-304)
   gossip_1b   same wrapper, one bucket (update after the whole backward)
   ddp_adam    torch DDP (bucketed NCCL all-reduce) + torch.optim.Adam(fused=True):
               the paper's All-Reduce baseline
@@ -47,7 +50,8 @@ def run(mode):
     cfg = dg.OptimizerConfig(alpha=1e-4, beta1=0.9, beta2=0.999, eps=1e-8)
     if mode.startswith("gossip"):
         net = DecentralizedDataParallel(model, topology=a.topology, optimizer=cfg,
-                                        bucket_cap_mb=25.0 if mode == "gossip" else 1e9)
+                                        bucket_cap_mb=1e9 if mode == "gossip_1b" else 25.0,
+                                        transport="nccl" if mode == "gossip_nccl" else "auto")
         opt = None
     elif mode == "ddp_adam":
         net = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
@@ -78,13 +82,14 @@ def run(mode):
     torch.cuda.synchronize()
     ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / a.iters], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    extra = f" buckets={len(net.buckets)}" if mode.startswith("gossip") else ""
+    extra = (f" buckets={len(net.buckets)} transport={ {1: 'nccl', 2: 'p2p'}[net.engine.stats()['transport']] }"
+             if mode.startswith("gossip") else "")
     del net, opt, model
     torch.cuda.empty_cache()
     return ms.item(), nparams, extra
 
 
-res = [(m, *run(m)) for m in ("local_adam", "ddp_adam", "gossip_1b", "gossip")]
+res = [(m, *run(m)) for m in ("local_adam", "ddp_adam", "gossip_1b", "gossip_nccl", "gossip")]
 if rank == 0:
     print(f"| mode ({world} B200, {res[0][2] / 1e6:.0f}M params, batch {a.batch}, {a.topology}) | ms / iteration |")
     print("|---|---|")

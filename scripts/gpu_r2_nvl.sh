@@ -37,3 +37,4 @@ for l in sys.stdin:
   done
   DG_LIB=$lib timeout 300 $TR --master-port 29632 scripts/xchg_bw.py --range --transport p2p --tag "$v" 2>&1 | grep -E "^xchg|rror" | head -2
 done
+timeout 900 $TR --master-port 29644 scripts/ddp_bench.py > gpurun_out/r2c_ddp_bench.log 2>&1; echo "ddp_bench rc=$?"; grep "^|" gpurun_out/r2c_ddp_bench.log
