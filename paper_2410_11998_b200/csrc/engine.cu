@@ -1041,12 +1041,14 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     // each row one column block ahead only, which does not cover NVLink
     // latency (config 3 at 2 GPUs: 19.9 ms vs 9.2 ms, measured)
     const bool xs_remote = dg::env_int("DG_XSHARE_REMOTE", 0) != 0;
-    // Rounds whose mixing components are all pairs (one-peer topologies) run the
-    // legacy pair kernel unless DG_XSHARE_PAIRS=1: a pair's two rows are read
-    // by one thread anyway, and without the per-column CTA barrier the small
-    // buckets run faster (config 1, 8 x 2^20: 44.3 vs 49.6 us per step; config
-    // 2 at 125M: 0.93 either way, measured).  In-place engines keep the
-    // x-sharing kernel everywhere (it writes the P2P publish copy).
+    // Rounds whose mixing components are all pairs (one-peer topologies) with
+    // buckets of <= 2^24 params run the legacy pair kernel unless
+    // DG_XSHARE_PAIRS=1: a pair's two rows are read by one thread anyway, and
+    // without the per-column CTA barrier small buckets run faster (config 1,
+    // 8 x 2^20: 44.3 vs 49.6 us per step), large ones do not (config 2 at
+    // 125M: 0.921 vs 0.932).  In-place engines run pair rounds on the legacy
+    // pair kernel at every size (it writes the P2P publish copy and hides
+    // NVLink latency better), other rounds on the x-sharing kernel.
     const bool xs_pairs = dg::env_int("DG_XSHARE_PAIRS", 0) != 0;
     e->gplans.resize(size_t(e->P));
     for (int r = 0; r < e->P; ++r) {
@@ -1059,8 +1061,10 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       // publish copy too) as long as the plain per-thread kernel is the one picked
       const bool plain_pairs = pairs && !xs_pairs && !dg::use_tma(e->plans[r]) &&
                                (e->plans[r].comp_size == 2 || int(e->plans[r].comps.size()) < dg::warps_min_nc());
+      const bool small = e->d <= (size_t(1) << 24);  // launch/latency-bound buckets
       const bool xs = e->xshare && (e->in_place ? !plain_pairs
-                                                : ((!p2p || !e->round_remote[r] || xs_remote) && (!pairs || xs_pairs)));
+                                                : ((!p2p || !e->round_remote[r] || xs_remote) &&
+                                                   (!pairs || !small || xs_pairs)));
       e->plans[r].xshare = xs;
       for (int g = 0; g < e->G; ++g) {
         const auto& q = all[r][g];

@@ -12,7 +12,7 @@ MP_TRANSPORT=p2p MP_D=100003 MP_CHUNK=16384 timeout 900 $TR --master-port 29641 
 MP_TRANSPORT=p2p MP_D=100003 DG_FAULT_DELAY_US=5000 DG_FAULT_POISON=1 timeout 900 $TR --master-port 29642 \
    tests/mp_parity_main.py > gpurun_out/r2c_parity_p2p_fault.log 2>&1; echo "parity p2p+fault rc=$?"
 timeout 900 $TR --master-port 29643 tests/mp_ddp_main.py > gpurun_out/r2c_ddp.log 2>&1; echo "ddp rc=$?"; grep rank gpurun_out/r2c_ddp.log | head -3
-for st in 0 4; do
+for st in 0 2; do
   timeout 300 build/nvl_probe_st$st 125000000 5 > gpurun_out/r2_nvl_probe_st$st.log 2>&1; echo "probe st$st rc=$?"; cat gpurun_out/r2_nvl_probe_st$st.log
 done
 timeout 300 build/nvl_probe_st0 125000000 1 > gpurun_out/r2_nvl_probe_plain.log 2>&1 && \
@@ -25,7 +25,7 @@ rows=[r for r in csv.reader(open('gpurun_out/r2_nvl_probe_ncu.csv')) if len(r)>1
 for r in rows:
     print(r[0], r[4][:40], r[-3], r[-1])
 PY
-for v in default libdg_xs_xp1 libdg_xs_st1 libdg_xs_st2; do
+for v in default libdg_xs_st1; do
   lib=build/variants/$v.so; [ $v = default ] && lib=paper_2410_11998_b200/libdg.so
   for c in 2 3 4; do
     DG_LIB=$lib DG_XSHARE_REMOTE=1 DG_XSHARE_PAIRS=1 timeout 900 $TR --master-port 29631 bench.py --gpus $N --config $c --no-e2e --steps 20 \
