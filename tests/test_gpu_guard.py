@@ -14,7 +14,7 @@ if not torch.cuda.is_available():
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LEGACY = {"DG_XSHARE": "0"}
-PATHS = {"default": {}, "xshare_pairs": {"DG_XSHARE_PAIRS": "1"}
+PATHS = {"default": {}, "xshare_pairs": {"DG_XSHARE_PAIRS": "1"},
          "legacy": {**LEGACY}, "pingpong": {**LEGACY, "DG_PINGPONG_MIN_NC": "1"},
          "tma": {**LEGACY, "DG_TMA": "2", "DG_PINGPONG_MIN_NC": "0"},
          "coop": {**LEGACY, "DG_TMA": "0", "DG_COOP_MIN_NC": "2", "DG_PINGPONG_MIN_NC": "0"},
