@@ -63,7 +63,7 @@ std::vector<double> dense(const dg_schedule& s, long round);
 dg_validation validate_dense(const std::vector<double>& w, int n);
 
 // ------------------------------------------------------------------ plans
-constexpr int kMaxLocal = 16;   // resident nodes per GPU
+constexpr int kMaxLocal = 64;   // resident nodes per GPU (64 x 125M x 16 B = 128 GB fits one B200)
 constexpr int kMaxDeg = 16;     // neighbours per node (self included)
 constexpr int kMaxRemote = kMaxLocal * kMaxDeg;  // distinct remote buckets per round per GPU (implied bound)
 

@@ -307,7 +307,7 @@ struct dg_engine {
   void harvest_timing();
   // times (optionally) and counts one launch of ours on the compute stream
   template <class F>
-  void timed(double bytes, double nvl_bytes, F&& launch);
+  void timed(double bytes, double nvl_bytes, F&& launch, int kernels = 1);
   std::vector<double> tev_remote;  // NVLink bytes read in-kernel per timed launch
   double remote_ms = 0, remote_bytes = 0;
   // bucketed steps (f1)
@@ -497,9 +497,22 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
     const size_t ri = size_t(&p - plans.data());
     if (ri >= gplans.size() || !gplans[ri].ok) throw dg::Error(DG_INVARIANT, "xshare: plan not owned by the engine");
     tp = &gplans[ri];
-  } else if (!tma) {
-    dg::fill_args(argbuf, p, bf, off, len, s, int(t), flag);
-    fn = dg::pick(p.comp_size, dg::launch_ns(p), algo, fold);
+  }
+  // legacy kernels take <= kSlots members per launch (FusedArgs): rounds with
+  // more components than that (> 16 resident nodes) run in batches
+  std::vector<dg::RoundPlan> batches;
+  if (!st_k && !tma) {
+    const size_t cmax = size_t(dg::kSlots / std::max(1, p.comp_size));
+    if (p.comps.size() > cmax) {
+      for (size_t c0 = 0; c0 < p.comps.size(); c0 += cmax) {
+        batches.push_back(p);
+        auto& q = batches.back();
+        q.comps.assign(p.comps.begin() + long(c0), p.comps.begin() + long(std::min(p.comps.size(), c0 + cmax)));
+      }
+    } else {
+      dg::fill_args(argbuf, p, bf, off, len, s, int(t), flag);
+      fn = dg::pick(p.comp_size, dg::launch_ns(p), algo, fold);
+    }
   }
   // algorithmic LOCAL HBM bytes of this launch (remote buckets: recv-slot reads
   // for NCCL; for P2P they come over NVLink and are counted in `received`)
@@ -513,14 +526,28 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   const double nvl = ((transport == DG_TRANSPORT_P2P && !slot_override) || xpub_out)
                          ? 4.0 * double(len) * double(p.recv_node.size())
                          : 0.0;
+#if DG_XS_IDX32
+  const size_t pieces = (len + (size_t(1) << 30) - 1) >> 30;  // launch_groups splits at 2^30 elements
+#else
+  const size_t pieces = 1;
+#endif
+  const int nk = st_k ? int(pieces) * ((int(tp->groups.size()) + dg::kShGroups - 1) / dg::kShGroups)
+                      : std::max<int>(1, int(batches.size()));
   timed(bytes, nvl, [&] {
-    if (st_k)
+    if (st_k) {
       launch_groups(*tp, x, xo, g, m, v, b, slot_ptr, off, len, s, fold, t, sms_for(p), xpub_out);
-    else if (tma)
+    } else if (tma) {
       dg::launch_tma(p, bf, algo, fold, off, len, s, int(t), flag, comp);
-    else
+    } else if (batches.empty()) {
       fn(argbuf.data(), (long long)(len / 4), int(p.comps.size()), sms_for(p), comp);
-  });
+    } else {
+      for (const auto& q : batches) {  // kernel parameters are copied at launch: argbuf is reusable
+        dg::fill_args(argbuf, q, bf, off, len, s, int(t), flag);
+        dg::pick(q.comp_size, dg::launch_ns(q), algo, fold)(argbuf.data(), (long long)(len / 4),
+                                                             int(q.comps.size()), sms_for(p), comp);
+      }
+    }
+  }, nk);
 }
 
 // One launch per (up to) kShGroups groups of the round; pointers at offset off.
@@ -592,14 +619,14 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
 }
 
 template <class F>
-void dg_engine::timed(double bytes, double nvl_bytes, F&& launch) {
+void dg_engine::timed(double bytes, double nvl_bytes, F&& launch, int kernels) {
   if (capturing) {  // recorded into a graph: no per-launch events, bytes kept for the replays
     launch();
     dg::cuda_check(cudaGetLastError(), "kernel launch (capture)");
-    ++cap_launches;
+    cap_launches += kernels;
     cap_hbm += bytes;
     cap_remote += nvl_bytes;
-    ++launches;
+    launches += kernels;
     hbm += bytes;
     return;
   }
@@ -620,10 +647,10 @@ void dg_engine::timed(double bytes, double nvl_bytes, F&& launch) {
   if (timing) {
     CU(cudaEventRecord(tev[tev_used].second, comp));
     tev_remote[tev_used] = nvl_bytes;
-    tev_n[tev_used] = 1;
+    tev_n[tev_used] = kernels;
     tev_bytes[tev_used++] = bytes;
   }
-  ++launches;
+  launches += kernels;
   hbm += bytes;
 }
 

@@ -207,7 +207,7 @@ dg::RoundPlan dg::build_round_plan(const dg_schedule& s, int world, int rank, lo
   RoundPlan p;
   const int first = first_node_of(rank, N, world), last = first_node_of(rank + 1, N, world);
   p.n_local = last - first;
-  if (p.n_local > kMaxLocal) config_error("plan: more than 16 resident nodes per GPU");
+  if (p.n_local > kMaxLocal) config_error("plan: more than 64 resident nodes per GPU");
   // distinct remote buckets needed here, ordered by (owner, node)
   std::vector<std::pair<int, int>> need;
   for (int i = first; i < last; ++i)

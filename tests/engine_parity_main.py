@@ -16,7 +16,9 @@ SEED = 2410
 TOPOS = [("make_one_peer_ring", "ONE_PEER_RING", (8,)), ("make_one_peer_exponential", "ONE_PEER_EXP", (8,)),
          ("make_static_exponential", "STATIC_EXP", (8,)), ("make_aer", "AER", (8, 2)),
          ("make_aer", "AER", (16, 4)), ("make_complete", "COMPLETE", (8,)),
-         ("make_static_exponential", "STATIC_EXP", (16,)), ("make_complete", "COMPLETE", (16,))]
+         ("make_static_exponential", "STATIC_EXP", (16,)), ("make_complete", "COMPLETE", (16,)),
+         # > 16 resident nodes: legacy rounds run in several launches (<= 16 members each)
+         ("make_one_peer_exponential", "ONE_PEER_EXP", (64,)), ("make_static_exponential", "STATIC_EXP", (32,))]
 CFG = {0: dict(alpha=2e-3, beta1=0.974, beta2=0.999, eps=1e-8, s=1),
        1: dict(alpha=8e-4, beta1=0.9, beta2=0.999, eps=1e-8, s=4)}
 

@@ -66,7 +66,7 @@ def main():
     T = 12
     bad = 0
     for fn, kind, args in CASES:
-        if -(-args[0] // world) > 16:  # engine limit: <= 16 resident nodes per GPU
+        if -(-args[0] // world) > 64:  # engine limit: <= 64 resident nodes per GPU
             continue
         for algo in (0, 1):
             obj = [dg.nccl_unique_id() if rank == 0 else None]

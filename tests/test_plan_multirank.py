@@ -34,10 +34,10 @@ def _worker(rank, world, port, q):
             n = s.workers()
             if world > n:
                 continue
-            if -(-n // world) > 16:  # engine limit: <= 16 resident nodes per GPU
+            if -(-n // world) > 64:  # engine limit: <= 64 resident nodes per GPU
                 try:
                     dg.plan_exchange(s, world, rank, 1)
-                    raise AssertionError("expected ConfigError for > 16 resident nodes")
+                    raise AssertionError("expected ConfigError for > 64 resident nodes")
                 except dg.ConfigError:
                     continue
             owner = [i * world // n for i in range(n)]
