@@ -603,7 +603,10 @@ def run_ours(a):
                         "kernel_ms_per_step": st["remote_kernel_ms"] / a.steps,
                         "what": "remote x^(t-1) buckets read in-kernel over NVLink by the exchange-round "
                                 "fused launches (per direction; every GPU both reads and serves)",
-                        "peak_source": "measured peer read bandwidth, B200_PROFILING.md (775 GB/s LDG.128)"}
+                        "peak_source": "measured peer read bandwidth, B200_PROFILING.md (775 GB/s LDG.128)",
+                        "hw_counters": ("NVML/nvidia-smi NVLink counters unsupported on this B200 pool; ncu "
+                                        "nvlrx__bytes of the same kernels in a single-process probe: "
+                                        "profiles/r2_nvl_probe.md (data bytes = 1.000x algorithmic, 715 GB/s)")}
                        if st["remote_kernel_ms"] > 0 else None),
             "nvlink_counters": nvl_counters,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,

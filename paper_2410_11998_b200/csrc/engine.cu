@@ -490,7 +490,7 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
                                                   : slots + (size_t(slot_set) * max_recv + r) * chunk;
   const dg::Buffers bf{slot_ptr, x, xo, g, m, v, algo == DG_ALGO_ACCUM ? b : nullptr, xpub_out};
   const bool st_k = p.xshare;
-  const bool tma = !st_k && dg::use_tma(p);
+  const bool tma = !st_k && dg::use_tma(p) && p.n_local <= dg::kSlots;  // TmaArgs holds <= 16 member rows
   dg::LaunchFn fn = nullptr;
   const dg::GroupPlan* tp = nullptr;
   if (st_k) {
@@ -1095,7 +1095,8 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       e->plans[r].xshare = xs;
       for (int g = 0; g < e->G; ++g) {
         const auto& q = all[r][g];
-        if (!xs && ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize)) pp = true;
+        // the legacy kernels take components of <= 16 members (FusedArgs / TmaArgs)
+        if (!xs && ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize || q.comp_size > dg::kSlots)) pp = true;
       }
       if (p2p && !e->in_place && e->round_remote[r]) pp = true;  // in place: peers read xpub instead
       if (pp && xs) {

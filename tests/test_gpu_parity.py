@@ -253,7 +253,7 @@ def test_engine_config_errors(dg):
     with pytest.raises(dg.ConfigError):
         eng.download(8, dg.X)
     with pytest.raises(dg.ConfigError):
-        dg.Engine(dg.make_one_peer_exponential(64), 100, dg.OptimizerConfig())  # 64 nodes on one GPU
+        dg.Engine(dg.make_one_peer_exponential(128), 100, dg.OptimizerConfig())  # > 64 nodes on one GPU
 
 
 def test_engine_upload_download_roundtrip(dg):
