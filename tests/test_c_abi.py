@@ -98,3 +98,31 @@ def test_engine_from_c_bit_exact(exe, oracle, tmp_path):
             pos += n * d
             assert np.array_equal(got.view(np.uint32), st[k].view(np.uint32)), (algo, k)
     assert pos == raw.size
+
+
+def test_cpp_adapter_compiles_and_matches_oracle(oracle, tmp_path):
+    """a declab-shaped C++20 adapter over dg.h (RAII
+    schedule, errors.hpp taxonomy) compiled with g++ and checked vs the oracle."""
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    exe = str(tmp_path / "cpp_adapter")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Werror", "-o", exe,
+                    os.path.join(ROOT, "tests", "cpp_adapter_main.cpp"), "-I", os.path.join(ROOT, "include"),
+                    "-L", LIBDIR, "-ldg", f"-Wl,-rpath,{LIBDIR}"], check=True)
+    makers = {"one_peer_exponential8": lambda: oracle.make_one_peer_exponential(8),
+              "aer8_2": lambda: oracle.make_aer(8, 2),
+              "static_exponential8": lambda: oracle.make_static_exponential(8)}
+    cur, rows = None, 0
+    out = run(exe)
+    for line in out:
+        f = line.split()
+        if f[0] == "schedule":
+            cur = makers[f[1]]()
+        elif f[0] == "round":
+            r, i = int(f[1]), int(f[3].rstrip(":"))
+            assert [int(x) for x in f[4:]] == list(cur.neighbors_at(r)[i][0]), line
+            rows += 1
+        elif f[0] == "validate":
+            assert f[-1] == "pass=1", line
+    assert rows == 8 * (3 + 4 + 1)
+    assert out[-1] == "error ConfigError"
