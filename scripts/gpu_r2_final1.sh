@@ -18,10 +18,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 600 $CMD > gpurun_out/r2f_short2.log 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:xshare -s 3 -c 1 \
     -o gpurun_out/r2f_config3_full $CMD > gpurun_out/r2f_ncu_full.log 2>&1; echo "ncu full rc=$?"
-for env in "DG_X=0" "DG_XSHARE=0" "DG_WAVES=2" "DG_PREFETCH=2"; do
-  env $env timeout 600 python bench.py --config 1 --no-cpu-baseline --no-e2e 2>&1 | grep "^{" | python -c "
+for c in 1 2 5; do
+  timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/r2f_bench_g1_c$c.log 2>&1; echo "bench config $c rc=$?"
+  grep "^{" gpurun_out/r2f_bench_g1_c$c.log | python -c "
 import json,sys
 for l in sys.stdin:
-    j=json.loads(l); print('config 1 $env', 'us/step', round(1e3*j['ms_per_step'],2), 'kfrac', round(j['roofline']['frac'],3), 'step', round(j['step_roofline']['frac'],3))
+    j=json.loads(l); print('config $c', 'value %.4e'%j['value'], 'ms', round(j['ms_per_step'],4), 'kfrac', round(j['roofline']['frac'],3), 'step', round(j['step_roofline']['frac'],3), 'e2e %.3e'%j['e2e']['value'], j['clocks'])
 "
 done
