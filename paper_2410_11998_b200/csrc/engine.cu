@@ -1069,7 +1069,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     // latency (config 3 at 2 GPUs: 19.9 ms vs 9.2 ms, measured)
     const bool xs_remote = dg::env_int("DG_XSHARE_REMOTE", 0) != 0;
     // Rounds whose mixing components are all pairs (one-peer topologies) with
-    // buckets of <= 2^24 params run the legacy pair kernel unless
+    // buckets of <= 2^24 params or fewer than 8 resident nodes run the legacy pair kernel unless
     // DG_XSHARE_PAIRS=1: a pair's two rows are read by one thread anyway, and
     // without the per-column CTA barrier small buckets run faster (config 1,
     // 8 x 2^20: 44.3 vs 49.6 us per step), large ones do not (config 2 at
@@ -1088,7 +1088,10 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       // publish copy too) as long as the plain per-thread kernel is the one picked
       const bool plain_pairs = pairs && !xs_pairs && !dg::use_tma(e->plans[r]) &&
                                (e->plans[r].comp_size == 2 || int(e->plans[r].comps.size()) < dg::warps_min_nc());
-      const bool small = e->d <= (size_t(1) << 24);  // launch/latency-bound buckets
+      // launch/latency-bound buckets, or too few resident nodes to fill the
+      // x-sharing CTAs (a group of one pair is a 2-warp CTA: config 2 at 4 GPUs,
+      // 2 nodes per GPU, ran 2.02 ms/step vs 1.43 ms on the legacy kernel)
+      const bool small = e->d <= (size_t(1) << 24) || e->NL < 8;
       const bool xs = e->xshare && (e->in_place ? !plain_pairs
                                                 : ((!p2p || !e->round_remote[r] || xs_remote) &&
                                                    (!pairs || !small || xs_pairs)));
