@@ -19,6 +19,7 @@ ap.add_argument("--bucket-params", dest="d", type=int, default=125_000_000)
 ap.add_argument("--topology", default="one_peer_exponential")
 ap.add_argument("--chunk", type=int, default=0)
 ap.add_argument("--periods", type=int, default=2)
+ap.add_argument("--b2b", action="store_true", help="steps back to back (no barrier/sync between them), events per step")
 a = ap.parse_args()
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
@@ -40,7 +41,23 @@ for _ in range(P):
     eng.step(t)
 eng.sync()
 res = {}
-for _ in range(a.periods * P):
+if a.b2b:   # the bench's regime: per-step events on the compute stream, no host sync in between
+    evs = []
+    dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(a.periods * P):
+        t += 1
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        eng.step(t)
+        e1.record(comp)
+        evs.append(((t - 1) % P + 1, e0, e1))
+    eng.sync()
+    for r, e0, e1 in evs:
+        ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        res.setdefault(r, []).append(ms.item())
+for _ in range(0 if a.b2b else a.periods * P):
     t += 1
     dist.barrier()
     torch.cuda.synchronize()
@@ -55,8 +72,9 @@ for _ in range(a.periods * P):
 if rank == 0:
     sends, recvs = {}, {}
     tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith(("DG_", "NCCL_P2P", "NCCL_MIN", "NCCL_MAX")))
-    line = " ".join(f"r{r}:{min(v):.2f}" for r, v in sorted(res.items()))
-    avg = sum(min(v) for v in res.values()) / len(res)
-    print(f"[{tag or 'default'}] chunk={a.chunk} rounds(ms) {line} avg={avg:.2f}", flush=True)
+    line = " ".join(f"r{r}:{min(v):.2f}/{sum(v) / len(v):.2f}/{max(v):.2f}" for r, v in sorted(res.items()))
+    avg = sum(sum(v) / len(v) for v in res.values()) / len(res)
+    print(f"[{tag or 'default'}]{' b2b' if a.b2b else ''} chunk={a.chunk} rounds(ms min/mean/max) {line} "
+          f"avg(mean)={avg:.2f}", flush=True)
 eng.close()
 dist.destroy_process_group()
