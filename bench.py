@@ -62,6 +62,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=4)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-clocks", action="store_true", help="do not sample nvidia-smi during the timed region")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
 
@@ -477,7 +478,7 @@ def run_ours(a):
     eng.sync()
 
     clocks = ClockSampler()
-    if rank == 0:
+    if rank == 0 and not a.no_clocks:
         clocks.start()
         time.sleep(0.3)
     # ---- timed region: K steps, CUDA events on the engine's compute stream
@@ -506,7 +507,7 @@ def run_ours(a):
     ms = ev0.elapsed_time(ev1)
     st = eng.stats()
     eng.set_timing(False)
-    clk = clocks.stop() if rank == 0 else None
+    clk = clocks.stop() if rank == 0 and not a.no_clocks else None
     ms_max = max_over_ranks(ms)
     launches = st["kernel_launches"] - launches0
     nvl_counters = None
