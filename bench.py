@@ -486,9 +486,9 @@ def run_ours(a):
     eng.set_timing(True)
     launches0 = eng.stats()["kernel_launches"]
     nvc = NvlCounters(local) if world > 1 else None
+    nv0 = nvc.read() if nvc else None   # (before the barrier: host work here would skew the ranks' start)
     barrier()
     torch.cuda.synchronize()
-    nv0 = nvc.read() if nvc else None
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(comp)
     timed_t = list(range(t + 1, t + a.steps + 1))
@@ -502,8 +502,8 @@ def run_ours(a):
     ev1.record(comp)
     eng.sync()
     torch.cuda.synchronize()
-    nv1 = nvc.read() if nvc else None
     barrier()
+    nv1 = nvc.read() if nvc else None
     ms = ev0.elapsed_time(ev1)
     st = eng.stats()
     eng.set_timing(False)

@@ -53,6 +53,10 @@ if a.b2b:   # the bench's regime: per-step events on the compute stream, no host
         e1.record(comp)
         evs.append(((t - 1) % P + 1, e0, e1))
     eng.sync()
+    tot = torch.tensor([evs[0][1].elapsed_time(evs[-1][2]) / len(evs)], device="cuda")
+    dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(f"b2b first-to-last per step (incl. gaps between steps): {tot.item():.3f} ms", flush=True)
     for r, e0, e1 in evs:
         ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
