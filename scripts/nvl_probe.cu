@@ -159,5 +159,82 @@ int main(int argc, char** argv) {
     }
   }
   CK(cudaDeviceSynchronize());
+
+  // ---- the f1 (DDP) in-place P2P range step, one node per GPU: each GPU's
+  // legacy pair kernel reads its own x and the peer's publish buffer over
+  // NVLink and writes x in place + its own publish copy.  Both GPUs at once
+  // (bidirectional NVLink traffic, as in training) and GPU 0 alone.
+  CK(cudaSetDevice(1));
+  CK(cudaDeviceEnablePeerAccess(0, 0));
+  float *ix[2], *ig[2], *im[2], *iv[2], *ipub[2][2];
+  cudaStream_t st[2];
+  cudaEvent_t b0[2], b1[2];
+  for (int dv = 0; dv < 2; ++dv) {
+    CK(cudaSetDevice(dv));
+    for (float** p : {&ix[dv], &ig[dv], &im[dv], &iv[dv], &ipub[dv][0], &ipub[dv][1]}) {
+      CK(cudaMalloc(p, bytes));
+      CK(cudaMemset(*p, 0, bytes));
+    }
+    CK(cudaStreamCreateWithFlags(&st[dv], cudaStreamNonBlocking));
+    CK(cudaEventCreate(&b0[dv]));
+    CK(cudaEventCreate(&b1[dv]));
+  }
+  auto args_for = [&](int dv) {
+    FusedArgs<1, 2> a{};
+    const int peer = 1 - dv;
+    a.src[0][dv] = ix[dv];            // ascending global id: node 0 then node 1
+    a.src[0][peer] = ipub[peer][0];   // peer's x^(t-1) publish buffer (over NVLink)
+    a.w[0][0][0] = a.w[0][0][1] = 0.5;
+    a.ns[0] = 2;
+    a.nm[0] = 1;
+    a.x[0][0] = ix[dv];
+    a.xp[0][0] = ipub[dv][1];
+    a.g[0][0] = ig[dv];
+    a.m[0][0] = im[dv];
+    a.v[0][0] = iv[dv];
+    a.s = s;
+    a.n = d;
+    a.t = 1;
+    a.div_flag = flag;
+    return a;
+  };
+  for (int both = 1; both >= 0; --both) {
+    float ms[2] = {0, 0};
+    for (int dv = 0; dv <= both; ++dv) {
+      CK(cudaSetDevice(dv));
+      auto k = gossip_adam_fused<1, 2, 0, false>;
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, LaunchShape<1, 2>::threads, 0));
+      const FusedArgs<1, 2> a = args_for(dv);
+      k<<<dim3(unsigned(occ * sms), 1), LaunchShape<1, 2>::threads, 0, st[dv]>>>(a);  // warm-up
+    }
+    for (int dv = 0; dv <= both; ++dv) {
+      CK(cudaSetDevice(dv));
+      CK(cudaStreamSynchronize(st[dv]));
+    }
+    for (int dv = 0; dv <= both; ++dv) {
+      CK(cudaSetDevice(dv));
+      auto k = gossip_adam_fused<1, 2, 0, false>;
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, LaunchShape<1, 2>::threads, 0));
+      const FusedArgs<1, 2> a = args_for(dv);
+      CK(cudaEventRecord(b0[dv], st[dv]));
+      for (int it = 0; it < iters; ++it) k<<<dim3(unsigned(occ * sms), 1), LaunchShape<1, 2>::threads, 0, st[dv]>>>(a);
+      CK(cudaEventRecord(b1[dv], st[dv]));
+    }
+    for (int dv = 0; dv <= both; ++dv) {
+      CK(cudaSetDevice(dv));
+      CK(cudaEventSynchronize(b1[dv]));
+      CK(cudaEventElapsedTime(&ms[dv], b0[dv], b1[dv]));
+      ms[dv] /= iters;
+      std::printf("in-place pair kernel (+publish), %s: GPU %d %.3f ms  local HBM %.0f GB/s  NVLink %.0f GB/s\n",
+                  both ? "both GPUs at once" : "GPU 0 alone      ", dv, ms[dv], 32.0 * d / ms[dv] / 1e6,
+                  4.0 * d / ms[dv] / 1e6);
+    }
+  }
+  for (int dv = 0; dv < 2; ++dv) {
+    CK(cudaSetDevice(dv));
+    CK(cudaDeviceSynchronize());
+  }
   return 0;
 }
