@@ -37,6 +37,11 @@
 
 using namespace dg;
 
+// plain float4 copy (one grid-stride pass): the NVLink read vs write probe
+__global__ void __launch_bounds__(256) copy4(float4* __restrict__ dst, const float4* __restrict__ src, long long n4) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += (long long)gridDim.x * 256) dst[i] = src[i];
+}
+
 int main(int argc, char** argv) {
   const long long d = argc > 1 ? atoll(argv[1]) : 125000000LL;  // params per node
   const int iters = argc > 2 ? atoi(argv[2]) : 5;
@@ -236,5 +241,30 @@ int main(int argc, char** argv) {
     CK(cudaSetDevice(dv));
     CK(cudaDeviceSynchronize());
   }
+  // ---- NVLink pull (remote reads) vs push (remote posted writes) of 0.5 GB,
+  // one GPU and both GPUs at once
+  for (int push = 0; push < 2; ++push)
+    for (int both = 0; both < 2; ++both) {
+      float ms[2] = {0, 0};
+      for (int rep = 0; rep < 2; ++rep) {  // rep 0 = warm-up
+        for (int dv = 0; dv <= both; ++dv) {
+          CK(cudaSetDevice(dv));
+          const int peer = 1 - dv;
+          float4* dst = reinterpret_cast<float4*>(push ? ipub[peer][1] : ipub[dv][1]);
+          const float4* src = reinterpret_cast<const float4*>(push ? ix[dv] : ipub[peer][0]);
+          CK(cudaEventRecord(b0[dv], st[dv]));
+          for (int it = 0; it < iters; ++it) copy4<<<unsigned(sms * 8), 256, 0, st[dv]>>>(dst, src, d / 4);
+          CK(cudaEventRecord(b1[dv], st[dv]));
+        }
+        for (int dv = 0; dv <= both; ++dv) {
+          CK(cudaSetDevice(dv));
+          CK(cudaEventSynchronize(b1[dv]));
+          CK(cudaEventElapsedTime(&ms[dv], b0[dv], b1[dv]));
+        }
+      }
+      for (int dv = 0; dv <= both; ++dv)
+        std::printf("NVLink %s, %s: GPU %d %.3f ms per 0.5 GB = %.0f GB/s\n", push ? "push (remote writes)" : "pull (remote reads) ",
+                    both ? "both GPUs" : "one GPU  ", dv, ms[dv] / iters, 4.0 * d / (ms[dv] / iters) / 1e6);
+    }
   return 0;
 }
