@@ -398,6 +398,13 @@ struct dg_engine {
   std::map<size_t, int> range_slot;         // range offset -> flag row (first-use order)
   std::map<size_t, long> range_last;        // last iteration stepped per range
   bool signal_kernel = false;
+  // push variant (DG_INPLACE_PUSH, default on when every resident node has at
+  // most one remote reader rank per round): the update kernel STORES x^(t)
+  // straight into the reader's receive slot over NVLink (posted writes) and
+  // reads its own neighbours' x^(t-1) from local slots; xpub[] are then the
+  // receive buffers [parity][recv slot][d_pad].  Same flags, same waits.
+  bool push = false;
+  std::vector<std::vector<std::pair<int, int>>> push_dst;  // [round][local node] -> (reader rank, its slot) or (-1,-1)
   static constexpr int kMaxRanges = 4096;
   void step_range_p2p(long t, size_t off, size_t len);
   void signal_range(int slot, unsigned long long value);
@@ -520,11 +527,11 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   // algorithmic LOCAL HBM bytes of this launch (remote buckets: recv-slot reads
   // for NCCL; for P2P they come over NVLink and are counted in `received`)
   const double per = algo == DG_ALGO_DADAM ? 28.0 : (fold ? 36.0 : 28.0);
-  const double remote_hbm = ((transport == DG_TRANSPORT_P2P && !slot_override) || xpub_out)
+  const double remote_hbm = ((transport == DG_TRANSPORT_P2P && !slot_override) || (xpub_out && !push))
                                 ? 0.0
                                 : 4.0 * double(p.recv_node.size());
-  // (+4 B per param for the in-place P2P publish copy of x^(t))
-  const double bytes = double(len) * ((per + (xpub_out ? 4.0 : 0.0)) * p.n_local + remote_hbm);
+  // (+4 B per param for the in-place P2P publish copy of x^(t); pushed copies land in peer HBM)
+  const double bytes = double(len) * ((per + (xpub_out && !push ? 4.0 : 0.0)) * p.n_local + remote_hbm);
   // NVLink bytes the launch reads in-kernel (P2P exchange rounds, in-place P2P ranges)
   const double nvl = ((transport == DG_TRANSPORT_P2P && !slot_override) || xpub_out)
                          ? 4.0 * double(len) * double(p.recv_node.size())
@@ -590,7 +597,7 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
       for (int q = 0; q < d.nl; ++q) {
         const int li = G.members[size_t(q)];
         d.xo[q] = xo[li] + off;
-        d.xp[q] = xp ? xp[li] + off : nullptr;
+        d.xp[q] = (xp && xp[li]) ? xp[li] + off : nullptr;
         d.g[q] = g[li] + off;
         d.m[q] = m[li] + off;
         d.v[q] = v[li] + off;
@@ -742,10 +749,19 @@ void dg_engine::step_range_p2p(long t, size_t off, size_t len) {
   const int slot = it->second;
   ++steps;
   const long last = range_last.count(off) ? range_last[off] : -1;
+  const size_t ri = size_t((t - 1) % P), ni = size_t(t % P);
   if (last != t - 1) {  // first step of this range (or a restart): publish x^(t-1)
-    for (int i = 0; i < NL; ++i)
-      CU(cudaMemcpyAsync(xpub[(t - 1) & 1] + size_t(i) * d_pad + off, buf(DG_BUF_X, i) + off, len * sizeof(float),
-                         cudaMemcpyDeviceToDevice, comp));
+    for (int i = 0; i < NL; ++i) {
+      if (push) {  // into the round-t readers' receive slots (peer copies)
+        const auto [q, sl] = push_dst[ri][size_t(i)];
+        if (q >= 0)
+          CU(cudaMemcpyAsync(peer_base[(t - 1) & 1][q] + size_t(sl) * d_pad + off, buf(DG_BUF_X, i) + off,
+                             len * sizeof(float), cudaMemcpyDeviceToDevice, comp));
+      } else {
+        CU(cudaMemcpyAsync(xpub[(t - 1) & 1] + size_t(i) * d_pad + off, buf(DG_BUF_X, i) + off,
+                           len * sizeof(float), cudaMemcpyDeviceToDevice, comp));
+      }
+    }
     signal_range(slot, (unsigned long long)t);
   }
   fault_delay(comp);
@@ -756,17 +772,30 @@ void dg_engine::step_range_p2p(long t, size_t off, size_t len) {
                                        reinterpret_cast<CUdeviceptr>(sig + size_t(slot) * G + r),
                                        (cuuint64_t)t, CU_STREAM_WAIT_VALUE_GEQ),
                    "cuStreamWaitValue64");
-  const dg::RoundPlan& p = plans[size_t((t - 1) % P)];
+  const dg::RoundPlan& p = plans[ri];
   std::vector<const float*> slot_ptr(std::max<size_t>(1, p.recv_node.size()));
   for (size_t r = 0; r < p.recv_node.size(); ++r) {
-    const int node = p.recv_node[r], owner = dg::owner_of(node, N, G);
-    slot_ptr[r] = peer_base[(t - 1) & 1][owner] + size_t(node - dg::first_node_of(owner, N, G)) * d_pad + off;
+    if (push) {  // pushed here by the owner at t-1
+      slot_ptr[r] = xpub[(t - 1) & 1] + r * d_pad + off;
+    } else {
+      const int node = p.recv_node[r], owner = dg::owner_of(node, N, G);
+      slot_ptr[r] = peer_base[(t - 1) & 1][owner] + size_t(node - dg::first_node_of(owner, N, G)) * d_pad + off;
+    }
   }
-  float* pub[dg::kMaxLocal];
-  for (int i = 0; i < NL; ++i) pub[i] = xpub[t & 1] + size_t(i) * d_pad;
+  float* pub[dg::kMaxLocal];  // (bases; the launch adds the range offset; null = no copy)
+  for (int i = 0; i < NL; ++i) {
+    if (push) {
+      const auto [q, sl] = push_dst[ni][size_t(i)];
+      pub[i] = q >= 0 ? peer_base[t & 1][q] + size_t(sl) * d_pad : nullptr;
+    } else {
+      pub[i] = xpub[t & 1] + size_t(i) * d_pad;
+    }
+  }
   sent += 4.0 * double(len) * double(p.send_node.size());
   received += 4.0 * double(len) * double(p.recv_node.size());
   if (!diag_skip_kernel) enqueue_fused(p, off, len, 0, s, fold, t, slot_ptr.data(), pub);
+  if (push)  // consumed receive slots: the owners refill this parity only after our t+1 signal
+    for (size_t r = 0; r < p.recv_node.size(); ++r) poison_range(xpub[(t - 1) & 1] + r * d_pad + off, len, comp);
   signal_range(slot, (unsigned long long)(t + 1));
   range_last[off] = t;
 }
@@ -1160,6 +1189,25 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     }
     e->inplace_p2p = p2p && e->in_place;
     e->signal_kernel = dg::env_int("DG_SIGNAL_KERNEL", 0) != 0;
+    if (e->inplace_p2p && dg::env_int("DG_INPLACE_PUSH", 1) != 0) {
+      // reader rank and receive slot of every resident node, per round (from
+      // every rank's plan); push only if each node has <= 1 remote reader rank
+      bool ok = true;
+      e->push_dst.assign(size_t(e->P), std::vector<std::pair<int, int>>(size_t(e->NL), {-1, -1}));
+      for (int r = 0; r < e->P && ok; ++r)
+        for (int g = 0; g < e->G && ok; ++g) {
+          if (g == e->rank) continue;
+          const auto& rn = all[r][g].recv_node;
+          for (size_t sl = 0; sl < rn.size(); ++sl) {
+            const int li = rn[sl] - e->first;
+            if (li < 0 || li >= e->NL) continue;
+            auto& dst = e->push_dst[size_t(r)][size_t(li)];
+            if (dst.first >= 0) ok = false;
+            dst = {g, int(sl)};
+          }
+        }
+      e->push = ok;
+    }
     CU(cudaSetDevice(c->device));
     e->sm_total = dg::sm_count(c->device);
     if (const char* rs = std::getenv("DG_RESERVE_SMS")) e->reserve_sms = std::max(0, std::atoi(rs));
@@ -1186,9 +1234,11 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       CU(cudaMemsetAsync(e->x_alt, 0, sizeof(float) * e->d_pad * e->NL, e->comp));
     }
     if (e->inplace_p2p) {
+      // pull: publish copies [node]; push: receive slots [slot] (written by the peers)
+      const size_t rows = e->push ? size_t(std::max(1, e->max_recv)) : size_t(e->NL);
       for (auto& pb : e->xpub) {
-        CU(cudaMalloc(&pb, sizeof(float) * e->d_pad * e->NL));
-        CU(cudaMemsetAsync(pb, 0, sizeof(float) * e->d_pad * e->NL, e->comp));
+        CU(cudaMalloc(&pb, sizeof(float) * e->d_pad * rows));
+        CU(cudaMemsetAsync(pb, 0, sizeof(float) * e->d_pad * rows, e->comp));
       }
       const size_t nsig = size_t(dg_engine::kMaxRanges) * e->G;
       CU(cudaMalloc(&e->sig, sizeof(unsigned long long) * nsig));
