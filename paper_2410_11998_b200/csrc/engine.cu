@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -406,6 +407,17 @@ struct dg_engine {
   bool push = false;
   std::vector<std::vector<std::pair<int, int>>> push_dst;  // [round][local node] -> (reader rank, its slot) or (-1,-1)
   static constexpr int kMaxRanges = 4096;
+  // P2P push exchange (DG_P2P_PUSH=1, engines that are not in place): every
+  // step's kernel also stores x^(t) of each resident node into the receive
+  // slots of its remote readers of round t+1 (posted NVLink writes), so every
+  // round reads only local memory and x is updated in place; a stream-ordered
+  // barrier before every step orders the slot parities.  x^(t-1) is seeded
+  // with peer copies before a step when x changed outside the engine.
+  bool p2p_push = false;
+  float* pbuf[2] = {};  // receive slots [parity][max_recv][d_pad], written by the peers
+  std::vector<std::vector<std::array<std::pair<int, int>, dg::kPushMax>>> pdst;  // [round][local] -> (rank, slot)
+  long seeded_for = -1;  // step whose x^(t-1) is in the readers' slots
+  void push_seed(long t);
   void step_range_p2p(long t, size_t off, size_t len);
   void signal_range(int slot, unsigned long long value);
   // CUDA graphs of whole step ranges (dg_engine_run_steps): small buckets are
@@ -451,6 +463,8 @@ dg_engine::~dg_engine() {
   for (int r = 0; r < int(peer_sig.size()); ++r)
     if (r != rank && peer_sig[r]) cudaIpcCloseMemHandle(peer_sig[r]);
   for (float* p : xpub)
+    if (p) cudaFree(p);
+  for (float* p : pbuf)
     if (p) cudaFree(p);
   if (sig) cudaFree(sig);
   for (int b = 0; b < 2; ++b)
@@ -527,11 +541,12 @@ void dg_engine::enqueue_fused(const dg::RoundPlan& p, size_t off, size_t len, in
   // algorithmic LOCAL HBM bytes of this launch (remote buckets: recv-slot reads
   // for NCCL; for P2P they come over NVLink and are counted in `received`)
   const double per = algo == DG_ALGO_DADAM ? 28.0 : (fold ? 36.0 : 28.0);
-  const double remote_hbm = ((transport == DG_TRANSPORT_P2P && !slot_override) || (xpub_out && !push))
+  const bool pushed = push || p2p_push;  // x^(t) copies stored into peers' slots, remote rows local
+  const double remote_hbm = ((transport == DG_TRANSPORT_P2P && !slot_override) || (xpub_out && !pushed))
                                 ? 0.0
                                 : 4.0 * double(p.recv_node.size());
   // (+4 B per param for the in-place P2P publish copy of x^(t); pushed copies land in peer HBM)
-  const double bytes = double(len) * ((per + (xpub_out && !push ? 4.0 : 0.0)) * p.n_local + remote_hbm);
+  const double bytes = double(len) * ((per + (xpub_out && !pushed ? 4.0 : 0.0)) * p.n_local + remote_hbm);
   // NVLink bytes the launch reads in-kernel (P2P exchange rounds, in-place P2P ranges)
   const double nvl = ((transport == DG_TRANSPORT_P2P && !slot_override) || xpub_out)
                          ? 4.0 * double(len) * double(p.recv_node.size())
@@ -597,7 +612,10 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
       for (int q = 0; q < d.nl; ++q) {
         const int li = G.members[size_t(q)];
         d.xo[q] = xo[li] + off;
-        d.xp[q] = (xp && xp[li]) ? xp[li] + off : nullptr;
+        for (int k = 0; k < dg::kPushMax; ++k) {
+          float* dst = xp ? xp[li * dg::kPushMax + k] : nullptr;
+          d.xp[q][k] = dst ? dst + off : nullptr;
+        }
         d.g[q] = g[li] + off;
         d.m[q] = m[li] + off;
         d.v[q] = v[li] + off;
@@ -782,13 +800,14 @@ void dg_engine::step_range_p2p(long t, size_t off, size_t len) {
       slot_ptr[r] = peer_base[(t - 1) & 1][owner] + size_t(node - dg::first_node_of(owner, N, G)) * d_pad + off;
     }
   }
-  float* pub[dg::kMaxLocal];  // (bases; the launch adds the range offset; null = no copy)
+  // [node][kPushMax] bases (the launch adds the range offset; null = no copy)
+  float* pub[dg::kMaxLocal * dg::kPushMax] = {};
   for (int i = 0; i < NL; ++i) {
     if (push) {
       const auto [q, sl] = push_dst[ni][size_t(i)];
-      pub[i] = q >= 0 ? peer_base[t & 1][q] + size_t(sl) * d_pad : nullptr;
+      pub[i * dg::kPushMax] = q >= 0 ? peer_base[t & 1][q] + size_t(sl) * d_pad : nullptr;
     } else {
-      pub[i] = xpub[t & 1] + size_t(i) * d_pad;
+      pub[i * dg::kPushMax] = xpub[t & 1] + size_t(i) * d_pad;
     }
   }
   sent += 4.0 * double(len) * double(p.send_node.size());
@@ -846,6 +865,20 @@ void dg_engine::step_range(long t, size_t off, size_t len) {
   }
 }
 
+// Peer copies of every resident node's current x (= x^(t-1)) into the slots
+// of its round-t remote readers (parity (t-1)&1), before step t's barrier.
+void dg_engine::push_seed(long t) {
+  const size_t ri = size_t((t - 1) % P);
+  for (int i = 0; i < NL; ++i)
+    for (int k = 0; k < dg::kPushMax; ++k) {
+      const auto [q, sl] = pdst[ri][size_t(i)][size_t(k)];
+      if (q < 0) continue;
+      CU(cudaMemcpyAsync(peer_base[(t - 1) & 1][q] + size_t(sl) * d_pad, buf(DG_BUF_X, i), d * sizeof(float),
+                         cudaMemcpyDeviceToDevice, comp));
+    }
+  seeded_for = t;
+}
+
 void dg_engine::step(long t) {
   if (!range_posted.empty())
     dg::config_error("step: bucketed exchanges are in flight (use dg_engine_step_range consistently)");
@@ -857,6 +890,34 @@ void dg_engine::step(long t) {
   if (inplace_p2p) return step_range_p2p(t, 0, d);
   ++steps;
   if (algo == DG_ALGO_ALLREDUCE) return step_allreduce(t, s);
+  if (transport == DG_TRANSPORT_P2P && G > 1 && p2p_push) {
+    if (seeded_for != t) push_seed(t);  // x^(t-1) into the round-t readers' slots
+    fault_delay(comp);
+    // every peer finished step t-1: its pushes of x^(t-1) into our slots of
+    // parity (t-1)&1 have landed, and it no longer reads its slots of parity
+    // t&1, which this step's kernel refills with x^(t)
+    NC(ncclAllReduce(bar_buf, bar_buf, 1, ncclFloat, ncclSum, nccl, comp));
+    ++barriers;
+    const size_t ni = size_t(t % P);
+    std::vector<const float*> slot_ptr(std::max<size_t>(1, p.recv_node.size()));
+    for (size_t r = 0; r < p.recv_node.size(); ++r) slot_ptr[r] = pbuf[(t - 1) & 1] + r * d_pad;
+    float* dst[dg::kMaxLocal * dg::kPushMax] = {};
+    size_t npush = 0;
+    for (int i = 0; i < NL; ++i)
+      for (int k = 0; k < dg::kPushMax; ++k) {
+        const auto [q, sl] = pdst[ni][size_t(i)][size_t(k)];
+        if (q < 0) continue;
+        dst[i * dg::kPushMax + k] = peer_base[t & 1][q] + size_t(sl) * d_pad;
+        ++npush;
+      }
+    sent += 4.0 * double(d) * double(npush);
+    received += 4.0 * double(d) * double(p.recv_node.size());
+    enqueue_fused(p, 0, d, 0, s, fold, t, slot_ptr.data(), npush ? dst : nullptr);
+    for (size_t r = 0; r < p.recv_node.size(); ++r) poison_range(pbuf[(t - 1) & 1] + r * d_pad, d, comp);
+    if (p.pingpong) xcur ^= 1;
+    seeded_for = t + 1;
+    return;
+  }
   if (transport == DG_TRANSPORT_P2P && G > 1) {
     // Cross-GPU step barrier, stream-ordered on the compute stream, before any
     // step that reads peers' x^(t-1) (their step t-1 must be complete) and
@@ -958,6 +1019,8 @@ dg_engine::GraphRec& dg_engine::capture(long t0, long t1) {
   // host-side bookkeeping that step() advances while capturing; restored
   // after, and re-applied on every replay
   const long l0 = launches, s0 = steps, b0 = barriers;
+  const long seed0 = seeded_for;
+  seeded_for = t0;  // P2P push: the seed copies stay outside the graph (run_steps issues them)
   const double h0 = hbm, se0 = sent, r0 = received;
   cap_hbm = cap_remote = 0;
   cap_launches = 0;
@@ -971,6 +1034,7 @@ dg_engine::GraphRec& dg_engine::capture(long t0, long t1) {
     cudaStreamEndCapture(comp, &g);
     if (g) cudaGraphDestroy(g);
     xcur = gr.x0;
+    seeded_for = seed0;
     launches = l0, steps = s0, barriers = b0, hbm = h0, sent = se0, received = r0;
     throw;
   }
@@ -978,6 +1042,7 @@ dg_engine::GraphRec& dg_engine::capture(long t0, long t1) {
   CU(cudaStreamEndCapture(comp, &g));
   gr.x1 = xcur;
   xcur = gr.x0;
+  seeded_for = seed0;
   gr.launches = launches - l0, gr.steps = steps - s0, gr.barriers = barriers - b0;
   gr.hbm = hbm - h0, gr.sent = sent - se0, gr.received = received - r0, gr.remote = cap_remote;
   launches = l0, steps = s0, barriers = b0, hbm = h0, sent = se0, received = r0;
@@ -999,6 +1064,7 @@ void dg_engine::run_steps(long t0, long t1, int flags) {
   }
   GraphRec& gr = capture(t0, t1);
   if (flags & DG_RUN_CAPTURE_ONLY) return;
+  if (p2p_push && seeded_for != t0) push_seed(t0);
   if (timing) {
     if (tev_used == tev.size()) {
       cudaEvent_t a, b;
@@ -1019,6 +1085,7 @@ void dg_engine::run_steps(long t0, long t1, int flags) {
     tev_n[tev_used++] = gr.launches;
   }
   xcur = gr.x1;
+  if (p2p_push) seeded_for = t1 + 1;
   launches += gr.launches, steps += gr.steps, barriers += gr.barriers;
   hbm += gr.hbm, sent += gr.sent, received += gr.received;
 }
@@ -1110,6 +1177,42 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     // NVLink latency better), other rounds on the x-sharing kernel.
     const bool xs_pairs = dg::env_int("DG_XSHARE_PAIRS", 0) != 0;
     e->gplans.resize(size_t(e->P));
+    // P2P push feasibility (every rank decides identically from the global plans):
+    // <= kPushMax reader ranks per node and round, and every round runs a
+    // kernel that stores the copies (x-sharing, or the plain legacy pair kernel)
+    bool want_push = p2p && !e->in_place && dg::env_int("DG_P2P_PUSH", 0) != 0;
+    if (want_push) {
+      e->pdst.assign(size_t(e->P), std::vector<std::array<std::pair<int, int>, dg::kPushMax>>(size_t(e->NL)));
+      for (auto& rr : e->pdst)
+        for (auto& a : rr) a.fill({-1, -1});
+      for (int r = 0; r < e->P && want_push; ++r) {
+        bool pairs = true;
+        for (int g = 0; g < e->G; ++g)
+          for (const auto& cp : all[r][g].comps) pairs = pairs && cp.members.size() <= 2 && cp.srcs.size() <= 2;
+        std::vector<int> readers(size_t(e->N), 0);  // remote reader ranks per node
+        for (int g = 0; g < e->G && want_push; ++g) {  // every rank's kernel must store the copies
+          const int nl_g = dg::first_node_of(g + 1, e->N, e->G) - dg::first_node_of(g, e->N, e->G);
+          const bool small = e->d <= (size_t(1) << 24) || nl_g < 8;
+          const bool xs = e->xshare && (!pairs || !small || xs_pairs);
+          const auto& q = all[r][g];
+          if (!xs && !(q.comp_size <= 2 && !dg::use_tma(q) &&
+                       (q.comp_size == 2 || int(q.comps.size()) < dg::warps_min_nc())))
+            want_push = false;
+          for (size_t sl = 0; sl < q.recv_node.size(); ++sl) {
+            const int node = q.recv_node[sl];
+            if (++readers[size_t(node)] > dg::kPushMax) want_push = false;
+            const int li = node - e->first;
+            if (li < 0 || li >= e->NL) continue;
+            auto& a = e->pdst[size_t(r)][size_t(li)];
+            int k = 0;
+            while (k < dg::kPushMax && a[size_t(k)].first >= 0) ++k;
+            if (k < dg::kPushMax) a[size_t(k)] = {g, int(sl)};
+          }
+        }
+      }
+      // (identical on every rank: every input above is global)
+    }
+    e->p2p_push = want_push;
     for (int r = 0; r < e->P; ++r) {
       bool pp = false, pairs = true;
       for (int g = 0; g < e->G; ++g) {
@@ -1125,7 +1228,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       // 2 nodes per GPU, ran 2.02 ms/step vs 1.43 ms on the legacy kernel)
       const bool small = e->d <= (size_t(1) << 24) || e->NL < 8;
       const bool xs = e->xshare && (e->in_place ? !plain_pairs
-                                                : ((!p2p || !e->round_remote[r] || xs_remote) &&
+                                                : ((!p2p || want_push || !e->round_remote[r] || xs_remote) &&
                                                    (!pairs || !small || xs_pairs)));
       e->plans[r].xshare = xs;
       for (int g = 0; g < e->G; ++g) {
@@ -1133,7 +1236,8 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
         // the legacy kernels take components of <= 16 members (FusedArgs / TmaArgs)
         if (!xs && ((pp_min > 0 && q.comp_size >= pp_min) || q.oversize || q.comp_size > dg::kSlots)) pp = true;
       }
-      if (p2p && !e->in_place && e->round_remote[r]) pp = true;  // in place: peers read xpub instead
+      // in place: peers read xpub; push: remote rows are local receive slots
+      if (p2p && !e->in_place && !want_push && e->round_remote[r]) pp = true;
       if (pp && xs) {
         // x-sharing kernel: in place on this GPU; only peers' readers (P2P
         // exchange rounds) need x^(t) in the other buffer
@@ -1176,7 +1280,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       const int pull_mode = pv ? std::atoi(pv) : 1;
       // in-kernel peer loads reach ~770 GB/s, copy-engine pulls ~420 GB/s (measured):
       // pull only when a remote bucket is read >= 1.75x on average
-      pr.pull = p2p && !e->in_place && !pr.recv_node.empty() &&
+      pr.pull = p2p && !e->in_place && !want_push && !pr.recv_node.empty() &&
                 (pull_mode == 2 || (pull_mode == 1 && 4 * remote_reads >= 7 * long(pr.recv_node.size())));
     }
     if (e->NL < 1) dg::config_error("engine_create: no resident nodes on this rank");
@@ -1229,10 +1333,15 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
       CU(cudaMalloc(&e->arena[k], sizeof(float) * e->d_pad * e->NL));
       CU(cudaMemsetAsync(e->arena[k], 0, sizeof(float) * e->d_pad * e->NL, e->comp));
     }
-    if ((any_pp || p2p) && !e->in_place) {
+    if ((any_pp || (p2p && !e->p2p_push)) && !e->in_place) {
       CU(cudaMalloc(&e->x_alt, sizeof(float) * e->d_pad * e->NL));
       CU(cudaMemsetAsync(e->x_alt, 0, sizeof(float) * e->d_pad * e->NL, e->comp));
     }
+    if (e->p2p_push)
+      for (auto& pb : e->pbuf) {
+        CU(cudaMalloc(&pb, sizeof(float) * e->d_pad * size_t(std::max(1, e->max_recv))));
+        CU(cudaMemsetAsync(pb, 0, sizeof(float) * e->d_pad * size_t(std::max(1, e->max_recv)), e->comp));
+      }
     if (e->inplace_p2p) {
       // pull: publish copies [node]; push: receive slots [slot] (written by the peers)
       const size_t rows = e->push ? size_t(std::max(1, e->max_recv)) : size_t(e->NL);
@@ -1272,8 +1381,8 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
     }
     for (int b = 0; b < 2; ++b) e->peer_base[b].assign(e->G, nullptr);
     // exported buffers: x and x_alt, or (in place) the two publish buffers + the flags
-    float* exp0 = e->inplace_p2p ? e->xpub[0] : e->arena[DG_BUF_X];
-    float* exp1 = e->inplace_p2p ? e->xpub[1] : e->x_alt;
+    float* exp0 = e->inplace_p2p ? e->xpub[0] : e->p2p_push ? e->pbuf[0] : e->arena[DG_BUF_X];
+    float* exp1 = e->inplace_p2p ? e->xpub[1] : e->p2p_push ? e->pbuf[1] : e->x_alt;
     e->peer_base[0][e->rank] = exp0;
     e->peer_base[1][e->rank] = exp1;
     e->peer_sig.assign(e->G, nullptr);
@@ -1353,6 +1462,7 @@ int dg_engine_create(const dg_engine_config* c, dg_engine** out) {
           }
         }
         e->inplace_p2p = false;
+        e->p2p_push = false;
         // every rank reaches this branch together (agreed flag)
         if (!auto_transport)
           dg::config_error("engine_create: P2P transport unavailable (CUDA IPC failed on some rank" +
@@ -1377,6 +1487,7 @@ int dg_engine_buffer(dg_engine* e, int local, int which, float** p) {
     if (local < 0 || local >= e->NL) dg::config_error("engine_buffer: local node out of range");
     if (which < 0 || which > 4 || !e->arena[which]) dg::config_error("engine_buffer: no such buffer");
     *p = e->buf(which, local);
+    if (which == DG_BUF_X) e->seeded_for = -1;  // the caller may write x: re-seed pushed copies
   });
 }
 
@@ -1391,6 +1502,7 @@ int dg_engine_upload(dg_engine* e, int local, int which, const float* host, size
   return guarded([&] {
     check_slice(e, local, which, off, cnt);
     CU(cudaSetDevice(e->device));
+    if (which == DG_BUF_X) e->seeded_for = -1;
     CU(cudaMemcpyAsync(e->buf(which, local) + off, host, cnt * sizeof(float), cudaMemcpyHostToDevice,
                        e->comp));
   });
@@ -1434,6 +1546,7 @@ int dg_engine_fill_synthetic(dg_engine* e, int which, uint64_t seed, uint32_t pu
   return guarded([&] {
     check_slice(e, 0, which, 0, 0);
     CU(cudaSetDevice(e->device));
+    if (which == DG_BUF_X) e->seeded_for = -1;
     for (int i = 0; i < e->NL; ++i) {
       const uint64_t st =
           dg::stream_state(seed, purpose, per_node ? uint64_t(e->first + i) : 0, iteration);

@@ -55,7 +55,7 @@ struct Buffers {
   float* const* m;
   float* const* v;
   float* const* b;  // null for DAdam
-  float* const* xpub = nullptr;  // in-place P2P publish copy of x^(t) (gossip_adam_fused only)
+  float* const* xpub = nullptr;  // [node][kPushMax] extra copies of x^(t) (gossip_adam_fused only)
 };
 
 // legacy.cu

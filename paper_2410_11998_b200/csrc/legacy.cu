@@ -134,7 +134,10 @@ void fill_args_t(std::vector<unsigned char>& buf, const RoundPlan& p, const Buff
       const int li = cp.members[j];
       for (size_t k = 0; k < cp.srcs.size(); ++k) a->w[c][j][k] = cp.w[j][k];
       a->x[c][j] = bf.xout[li] + off;
-      a->xp[c][j] = (bf.xpub && bf.xpub[li]) ? bf.xpub[li] + off : nullptr;
+      for (int k = 0; k < kPushMax; ++k) {
+        float* dst = bf.xpub ? bf.xpub[li * kPushMax + k] : nullptr;
+        a->xp[c][j][k] = dst ? dst + off : nullptr;
+      }
       a->g[c][j] = bf.g[li] + off;
       a->m[c][j] = bf.m[li] + off;
       a->v[c][j] = bf.v[li] + off;

@@ -50,7 +50,7 @@ struct ShGroup {
   const float* row[kShRows];          // x^(t-1) source rows (resident, peer or recv slot)
   double wrow[kShRows];               // COLW: the weight every reader of row r uses
   float* xo[kShNodes];                // where member q's x^(t) goes
-  float* xp[kShNodes];                // optional second copy of x^(t) (in-place P2P publish buffer)
+  float* xp[kShNodes][kPushMax];      // extra copies of x^(t) (publish buffer / peers' receive slots)
   const float* g[kShNodes];
   float* m[kShNodes];
   float* v[kShNodes];
@@ -164,7 +164,13 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
   const bool pf_x = conv && (gp.local_rows >> w & 1);  // resident row: prefetchable into L2
   const float* gq = member ? gp.g[w] : nullptr;
   float* xq = member ? gp.xo[w] : nullptr;
-  float* xpq = member ? gp.xp[w] : nullptr;
+  // extra x^(t) copies: pointers stay in the constant bank (read at the store)
+  const bool any_xp = member && (gp.xp[w][0] || gp.xp[w][1] || gp.xp[w][2] || gp.xp[w][3]);
+  auto store_xp = [&](idx_t e, const float4& x) {
+#pragma unroll
+    for (int k = 0; k < kPushMax; ++k)
+      if (gp.xp[w][k]) st4(gp.xp[w][k] + e, x);
+  };
   float* mq = member ? gp.m[w] : nullptr;
   float* vq = member ? gp.v[w] : nullptr;
   float* bq = member ? gp.b[w] : nullptr;
@@ -376,7 +382,7 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         bad |= !ok;
 #endif
         st4(xq + e, x);
-        if (xpq) st4(xpq + e, x);
+        if (any_xp) store_xp(e, x);
         st4_mv(mq + e, m);
         st4_mv(vq + e, v);
       } else {
@@ -401,7 +407,7 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         bad |= !ok;
 #endif
         st4(xq + e, x);
-        if (xpq) st4(xpq + e, x);
+        if (any_xp) store_xp(e, x);
         st4_mv(bq + e, bb);
         if (FOLD) {
           st4_mv(mq + e, m);
@@ -449,7 +455,10 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         }
       }
       xq[e] = x;
-      if (xpq) xpq[e] = x;
+      if (any_xp)
+#pragma unroll
+        for (int k = 0; k < kPushMax; ++k)
+          if (gp.xp[w][k]) gp.xp[w][k][e] = x;
     }
   }
   report_divergence(bad, a.t, a.div_flag);
