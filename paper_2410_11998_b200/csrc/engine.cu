@@ -893,12 +893,15 @@ void dg_engine::step(long t) {
   if (transport == DG_TRANSPORT_P2P && G > 1 && p2p_push) {
     if (seeded_for != t) push_seed(t);  // x^(t-1) into the round-t readers' slots
     fault_delay(comp);
-    // every peer finished step t-1: its pushes of x^(t-1) into our slots of
-    // parity (t-1)&1 have landed, and it no longer reads its slots of parity
-    // t&1, which this step's kernel refills with x^(t)
-    NC(ncclAllReduce(bar_buf, bar_buf, 1, ncclFloat, ncclSum, nccl, comp));
-    ++barriers;
+    // Barrier (every peer finished step t-1) before a step that reads its
+    // receive slots (round t remote: the peers' pushes of x^(t-1) have landed)
+    // or pushes (round t+1 remote: no peer still reads the parity t&1 slots
+    // this kernel refills -- their last reader ran before this barrier).
     const size_t ni = size_t(t % P);
+    if (round_remote[ri] || round_remote[ni]) {
+      NC(ncclAllReduce(bar_buf, bar_buf, 1, ncclFloat, ncclSum, nccl, comp));
+      ++barriers;
+    }
     std::vector<const float*> slot_ptr(std::max<size_t>(1, p.recv_node.size()));
     for (size_t r = 0; r < p.recv_node.size(); ++r) slot_ptr[r] = pbuf[(t - 1) & 1] + r * d_pad;
     float* dst[dg::kMaxLocal * dg::kPushMax] = {};
