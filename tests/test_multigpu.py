@@ -26,14 +26,15 @@ def _port():
 
 @pytest.mark.parametrize("world", sorted({2, min(4, torch.cuda.device_count())}))
 @pytest.mark.parametrize("d,chunk", [(100_003, 16384), (1 << 20, 0)])
-@pytest.mark.parametrize("transport", ["p2p", "nccl", "p2p_pull_always", "p2p_direct_only", "p2p_inplace_pull"])
+@pytest.mark.parametrize("transport", ["p2p", "nccl", "p2p_pull_always", "p2p_direct_only", "p2p_inplace_pull",
+                                       "p2p_push"])
 def test_multigpu_bit_exact(world, d, chunk, transport):
     if world > torch.cuda.device_count():
         pytest.skip("not enough GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_parity_main.py")]
     extra = {"p2p_pull_always": {"DG_P2P_PULL": "2"}, "p2p_direct_only": {"DG_P2P_PULL": "0"},
-             "p2p_inplace_pull": {"DG_INPLACE_PUSH": "0"}}.get(transport, {})
+             "p2p_inplace_pull": {"DG_INPLACE_PUSH": "0"}, "p2p_push": {"DG_P2P_PUSH": "1"}}.get(transport, {})
     env = {**os.environ, "MP_D": str(d), "MP_CHUNK": str(chunk), "MP_TRANSPORT": transport.split("_")[0], **extra}
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
@@ -42,7 +43,8 @@ def test_multigpu_bit_exact(world, d, chunk, transport):
 FAULT = {"DG_FAULT_DELAY_US": "5000", "DG_FAULT_RANK": "1", "DG_FAULT_POISON": "1"}
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl", "p2p_pull_always", "p2p_direct_only", "p2p_inplace_pull"])
+@pytest.mark.parametrize("transport", ["p2p", "nccl", "p2p_pull_always", "p2p_direct_only", "p2p_inplace_pull",
+                                       "p2p_push"])
 def test_exchange_protocol_under_fault_injection(transport):
     """SPEC.md:309/317/403: rank 1 runs 5 ms behind on every step (alternately
     before the cross-GPU barrier -- a late writer -- and after it -- a late
@@ -53,7 +55,7 @@ def test_exchange_protocol_under_fault_injection(transport):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_parity_main.py")]
     extra = {"p2p_pull_always": {"DG_P2P_PULL": "2"}, "p2p_direct_only": {"DG_P2P_PULL": "0"},
-             "p2p_inplace_pull": {"DG_INPLACE_PUSH": "0"}}.get(transport, {})
+             "p2p_inplace_pull": {"DG_INPLACE_PUSH": "0"}, "p2p_push": {"DG_P2P_PUSH": "1"}}.get(transport, {})
     env = {**os.environ, "MP_D": "100003", "MP_CHUNK": "16384", "MP_TRANSPORT": transport.split("_")[0],
            **extra, **FAULT}
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
