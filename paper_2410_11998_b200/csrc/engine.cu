@@ -222,9 +222,9 @@ GroupPlan build_group_plan(const RoundPlan& p) {
   return gp;
 }
 
-template <int DEG, int ALGO, bool FOLD, bool COLW>
+template <int DEG, int ALGO, bool FOLD, bool COLW, bool XP>
 void launch_xshare_t(const ShArgs& a, int ngroups, int warps, int sms, cudaStream_t st) {
-  auto kern = gossip_adam_xshare<DEG, ALGO, FOLD, COLW>;
+  auto kern = gossip_adam_xshare<DEG, ALGO, FOLD, COLW, XP>;
   constexpr size_t dyn = xshare_dyn_smem<DEG, ALGO>();
   static std::map<int, int> occ_of;  // resident CTAs per SM by CTA size
   int& occ = occ_of[warps];
@@ -241,12 +241,18 @@ void launch_xshare_t(const ShArgs& a, int ngroups, int warps, int sms, cudaStrea
 }
 
 void launch_xshare(const ShArgs& a, int ngroups, int warps, int max_deg, bool colw, int algo, bool fold,
-                   int sms, cudaStream_t st) {
-#define DG_XS_C(D, A, F)                                           \
-  if (colw) {                                                      \
-    return launch_xshare_t<D, A, F, true>(a, ngroups, warps, sms, st);  \
-  } else {                                                         \
-    return launch_xshare_t<D, A, F, false>(a, ngroups, warps, sms, st); \
+                   int sms, cudaStream_t st, bool xp) {
+#define DG_XS_X(D, A, F, C)                                            \
+  if (xp) {                                                            \
+    return launch_xshare_t<D, A, F, C, true>(a, ngroups, warps, sms, st);  \
+  } else {                                                             \
+    return launch_xshare_t<D, A, F, C, false>(a, ngroups, warps, sms, st); \
+  }
+#define DG_XS_C(D, A, F) \
+  if (colw) {            \
+    DG_XS_X(D, A, F, true)  \
+  } else {               \
+    DG_XS_X(D, A, F, false) \
   }
 #define DG_XS_D(A, F)   \
   if (max_deg <= 2) {   \
@@ -267,6 +273,7 @@ void launch_xshare(const ShArgs& a, int ngroups, int warps, int max_deg, bool co
   }
 #undef DG_XS_D
 #undef DG_XS_C
+#undef DG_XS_X
 }
 
 }  // namespace
@@ -641,7 +648,11 @@ void dg_engine::launch_groups(const dg::GroupPlan& tp, float* const* x, float* c
     a.prefetch = dg::xshare_prefetch();
     a.contiguous = dg::env_int("DG_XS_CONTIG", 0) != 0;
     a.div_flag = flag;
-    dg::launch_xshare(a, cnt, warps, tp.max_deg, tp.colw, algo, fold, sms, comp);
+    bool has_xp = false;
+    for (int k = 0; k < cnt; ++k)
+      for (int q = 0; q < a.grp[k].nl; ++q)
+        for (int j = 0; j < dg::kPushMax; ++j) has_xp |= a.grp[k].xp[q][j] != nullptr;
+    dg::launch_xshare(a, cnt, warps, tp.max_deg, tp.colw, algo, fold, sms, comp, has_xp);
   }
   }
 }

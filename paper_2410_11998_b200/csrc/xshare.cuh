@@ -128,7 +128,11 @@ constexpr size_t xshare_dyn_smem() {
              ? size_t(kShNodes) * 3 * (ALGO == 1 ? 4 : 3) * 32 * 16
              : 0;
 }
-template <int DEG, int ALGO, bool FOLD, bool COLW>
+// XP: members may store extra copies of x^(t) (ShGroup::xp: in-place P2P
+// publish buffer or push receive slots).  A separate instantiation, so the
+// plain kernel carries none of it (the copy pointers cost registers: config 3
+// ran 13.67 vs 13.00 ms with them compiled in).
+template <int DEG, int ALGO, bool FOLD, bool COLW, bool XP = false>
 __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(const __grid_constant__ ShArgs a) {
   __shared__ double2 P[2 * kShBufD2];
   constexpr bool kFastDir = DG_XS_FASTDIV == 1 || (DG_XS_FASTDIV == 2 && DEG >= 4);
@@ -165,7 +169,7 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
   const float* gq = member ? gp.g[w] : nullptr;
   float* xq = member ? gp.xo[w] : nullptr;
   // extra x^(t) copies: pointers stay in the constant bank (read at the store)
-  const bool any_xp = member && (gp.xp[w][0] || gp.xp[w][1] || gp.xp[w][2] || gp.xp[w][3]);
+  const bool any_xp = XP && member && (gp.xp[w][0] || gp.xp[w][1] || gp.xp[w][2] || gp.xp[w][3]);
   auto store_xp = [&](idx_t e, const float4& x) {
 #pragma unroll
     for (int k = 0; k < kPushMax; ++k)
@@ -382,7 +386,9 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         bad |= !ok;
 #endif
         st4(xq + e, x);
-        if (any_xp) store_xp(e, x);
+        if constexpr (XP) {
+          if (any_xp) store_xp(e, x);
+        }
         st4_mv(mq + e, m);
         st4_mv(vq + e, v);
       } else {
@@ -407,7 +413,9 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         bad |= !ok;
 #endif
         st4(xq + e, x);
-        if (any_xp) store_xp(e, x);
+        if constexpr (XP) {
+          if (any_xp) store_xp(e, x);
+        }
         st4_mv(bq + e, bb);
         if (FOLD) {
           st4_mv(mq + e, m);
@@ -455,10 +463,12 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
         }
       }
       xq[e] = x;
-      if (any_xp)
+      if constexpr (XP) {
+        if (any_xp)
 #pragma unroll
-        for (int k = 0; k < kPushMax; ++k)
-          if (gp.xp[w][k]) gp.xp[w][k][e] = x;
+          for (int k = 0; k < kPushMax; ++k)
+            if (gp.xp[w][k]) gp.xp[w][k][e] = x;
+      }
     }
   }
   report_divergence(bad, a.t, a.div_flag);
