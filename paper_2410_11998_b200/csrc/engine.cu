@@ -225,19 +225,16 @@ GroupPlan build_group_plan(const RoundPlan& p) {
 template <int DEG, int ALGO, bool FOLD, bool COLW, bool XP>
 void launch_xshare_t(const ShArgs& a, int ngroups, int warps, int sms, cudaStream_t st) {
   auto kern = gossip_adam_xshare<DEG, ALGO, FOLD, COLW, XP>;
-  constexpr size_t dyn = xshare_dyn_smem<DEG, ALGO>();
   static std::map<int, int> occ_of;  // resident CTAs per SM by CTA size
   int& occ = occ_of[warps];
   if (!occ) {
-    if (dyn) cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)),
-                        "xshare smem attribute");
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * warps, dyn), "xshare occupancy");
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * warps, 0), "xshare occupancy");
     occ = std::max(1, occ);
   }
   const long long blocks = std::max(1LL, ((a.n >> 2) + 31) / 32);
   const long long resident = std::max(1LL, (long long)(grid_waves() * occ * sms) / ngroups);
   dim3 grid(unsigned(std::min(blocks, resident)), unsigned(ngroups));
-  kern<<<grid, 32 * warps, dyn, st>>>(a);
+  kern<<<grid, 32 * warps, 0, st>>>(a);
 }
 
 void launch_xshare(const ShArgs& a, int ngroups, int warps, int max_deg, bool colw, int algo, bool fold,

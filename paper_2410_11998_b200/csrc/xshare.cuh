@@ -111,9 +111,6 @@ __device__ __forceinline__ void prefetch_l2_line(const void* p) {
 #ifndef DG_XS_STAGE
 #define DG_XS_STAGE 2    // > 0: x rows staged that many column blocks ahead (cp.async ring)
 #endif
-#ifndef DG_XS_GSTAGE
-#define DG_XS_GSTAGE 0   // 1: g/m/v also staged (cp.async, dynamic smem) in DAdam staged kernels; 2: also AccumAdam
-#endif
 #ifndef DG_XS_IDX32
 #define DG_XS_IDX32 1    // 1: 32-bit column indices (the host splits launches at 2^30 elements)
 #endif
@@ -121,17 +118,9 @@ __device__ __forceinline__ void prefetch_l2_line(const void* p) {
 #ifndef DG_XS_MINB
 #define DG_XS_MINB 3  // resident CTAs per SM the register budget is sized for
 #endif
-// dynamic shared memory of one instantiation (the g/m/v staging ring)
-template <int DEG, int ALGO>
-constexpr size_t xshare_dyn_smem() {
-  return (DEG >= 4 && DG_XS_STAGE > 0 && DG_XS_GSTAGE && (ALGO == 0 || DG_XS_GSTAGE > 1))
-             ? size_t(kShNodes) * 3 * (ALGO == 1 ? 4 : 3) * 32 * 16
-             : 0;
-}
 // XP: members may store extra copies of x^(t) (ShGroup::xp: in-place P2P
 // publish buffer or push receive slots).  A separate instantiation, so the
-// plain kernel carries none of it (the copy pointers cost registers: config 3
-// ran 13.67 vs 13.00 ms with them compiled in).
+// plain kernel carries none of it.
 template <int DEG, int ALGO, bool FOLD, bool COLW, bool XP = false>
 __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(const __grid_constant__ ShArgs a) {
   __shared__ double2 P[2 * kShBufD2];
@@ -249,43 +238,9 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  // g, m, v[, acc] of the member staged kG column blocks ahead the same way
-  // (dynamic shared memory [warp][slot][stream][lane]); the x and g/m/v copies
-  // of an iteration share one commit group, so wait_group kStage - kG covers
-  // both (x of block i was issued kStage iterations ago, g/m/v kG).
-  constexpr int kG = (kStage > 0 && DG_XS_GSTAGE && (ALGO == 0 || DG_XS_GSTAGE > 1)) ? 1 : 0;
-  constexpr int kGSlots = kG + 2, kNSt = ALGO == 1 ? 4 : 3;
-  extern __shared__ __align__(16) float4 GMV[];
-  const uint32_t gmv_base = uint32_t(__cvta_generic_to_shared(&GMV[(w * kGSlots * kNSt) * 32 + lane]));
-  auto gstage = [&](idx_t i) {
-    if (kG > 0 && member && i < count) {
-      const idx_t qi = ((first + i * step) << 5) + lane;
-      const bool ok = qi < n4;
-      const idx_t eo = ok ? qi << 2 : 0;
-      const int bytes = ok ? 16 : 0;
-      const uint32_t d0 = gmv_base + uint32_t(i % kGSlots) * uint32_t(kNSt) * 32u * 16u;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d0), "l"(gq + eo), "r"(bytes) : "memory");
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d0 + 512u), "l"(mq + eo), "r"(bytes) : "memory");
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d0 + 1024u), "l"(vq + eo), "r"(bytes) : "memory");
-      if (ALGO == 1)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d0 + 1536u), "l"(bq + eo), "r"(bytes) : "memory");
-    }
-  };
   if constexpr (kStage > 0) {
 #pragma unroll
-    for (int j = 0; j < kStage; ++j) {
-      if (conv) {  // (inline of stage() without its commit, so g/m/v join the group)
-        const idx_t qi = ((first + idx_t(j) * step) << 5) + lane;
-        if (idx_t(j) < count) {
-          const uint32_t dst = xr_base + uint32_t(j % kSlots) * 32u * 16u;
-          const float* src = qi < n4 ? xr + (qi << 2) : xr;
-          const int bytes = qi < n4 ? 16 : 0;
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
-        }
-      }
-      if (j < kG) gstage(idx_t(j));
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
+    for (int j = 0; j < kStage; ++j) stage(idx_t(j));
   }
 #if DG_XS_XPIPE
   // x^(t-1) row loaded one column block ahead: the conversion below never
@@ -301,7 +256,7 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
     const bool live = q < n4;  // false only for lanes of the last column block
     const idx_t e = q << 2;
     float4 g, m, v, bb;
-    if (kG == 0 && member && live) {
+    if (member && live) {
       g = ld_stream(gq + e);
       m = ld4(mq + e);
       v = ld4(vq + e);
@@ -309,9 +264,8 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
     }
     double2* Pb = P + buf * kShBufD2;
     if constexpr (kStage > 0) {
-      if constexpr (kG > 0) gstage(i + kG);
-      stage(i + kStage);  // (commits the group)
-      asm volatile("cp.async.wait_group %0;" ::"n"(kStage - kG) : "memory");  // block i has landed
+      stage(i + kStage);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kStage) : "memory");  // block i has landed
     }
     if (conv) {
       float4 x;
@@ -338,13 +292,6 @@ __global__ void __launch_bounds__(32 * kShNodes, DG_XS_MINB) gossip_adam_xshare(
     }
     __syncthreads();  // table complete; the other buffer's readers are one barrier back
     if (member && live) {
-      if constexpr (kG > 0) {
-        const float4* gs = &GMV[((w * kGSlots + int(i % kGSlots)) * kNSt) * 32 + lane];
-        g = gs[0];
-        m = gs[32];
-        v = gs[64];
-        if (ALGO == 1) bb = gs[96];
-      }
       double ax = 0.0, ay = 0.0, az = 0.0, aw = 0.0;
 #pragma unroll
       for (int k = 0; k < DEG; ++k) {
