@@ -50,7 +50,9 @@ struct ShGroup {
   const float* row[kShRows];          // x^(t-1) source rows (resident, peer or recv slot)
   double wrow[kShRows];               // COLW: the weight every reader of row r uses
   float* xo[kShNodes];                // where member q's x^(t) goes
+#if !DG_XS_XP_LAST
   float* xp[kShNodes][kPushMax];      // extra copies of x^(t) (publish buffer / peers' receive slots)
+#endif
   const float* g[kShNodes];
   float* m[kShNodes];
   float* v[kShNodes];
@@ -61,6 +63,9 @@ struct ShGroup {
   int deg[kShNodes];
   int nl, nx;
   unsigned local_rows;                // bit r: row r is a resident bucket (L2-prefetchable)
+#if DG_XS_XP_LAST
+  float* xp[kShNodes][kPushMax];      // extra copies of x^(t) (publish buffer / peers' receive slots)
+#endif
 };
 struct ShArgs {
   ShGroup grp[kShGroups];
