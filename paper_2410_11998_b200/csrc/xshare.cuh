@@ -110,11 +110,11 @@ __device__ __forceinline__ void prefetch_l2_line(const void* p) {
 #ifndef DG_XS_FASTDIV
 #define DG_XS_FASTDIV 2  // 1: branch-free 4-wide Adam direction (adam_dir4); 2: when DEG >= 4; 0: never
 #endif
-// x rows staged 2 column blocks ahead (measured, same sweep): config 3 0.908 -> 0.923,
-// static AccumAdam 0.927 -> 0.930, AER AccumAdam 0.960 -> 0.965; 1 block 0.877 / 0.933 /
-// 0.970, 4 blocks 0.834 on config 3; x one block ahead in registers (DG_XS_XPIPE) 0.816.
+// x rows staged 2 column blocks ahead measured 0.908 -> 0.923 on config 3 in one sweep
+// (sweep 3) but 0.905 -> 0.880 in the final build (sweep 6, same box class), so staging is
+// off by default; 4 blocks 0.834; x one block ahead in registers (DG_XS_XPIPE) 0.816.
 #ifndef DG_XS_STAGE
-#define DG_XS_STAGE 2    // > 0: x rows staged that many column blocks ahead (cp.async ring)
+#define DG_XS_STAGE 0    // > 0: x rows staged that many column blocks ahead (cp.async ring)
 #endif
 #ifndef DG_XS_IDX32
 #define DG_XS_IDX32 1    // 1: 32-bit column indices (the host splits launches at 2^30 elements)
